@@ -1,0 +1,408 @@
+"""Benchmark: useful GMAC/s of the unified segregated transpose convolution on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+A step is one forward pass of every layer of the workload over one synthetic
+batch (per GPU; weak scaling across ranks: batch sharding needs no collective).
+Default workload: the EB-GAN generator layers l2..l7 (reference GAN_SUITE,
+bench.py:133-138) at batch 256 per GPU in bf16 (fp32 accumulation), the
+BASELINE "EB-GAN generator transpose-conv layers, batch 256" configuration.
+
+value    useful MACs (analysis.py:46-57 mult_count_segregated x batch, all ranks)
+         / device time of the step (CUDA events, max over ranks), inputs resident.
+e2e      the same metric through the public API (PreparedLayer.forward) with
+         pinned HOST input/output tensors: H2D + compute + D2H inside the region.
+roofline dominant kernel (largest share of the step): algorithmic bytes/flops per
+         launch / its average event-timed duration vs MEASURED_PEAKS.
+cpu_baseline  the CPU oracle port of the reference's segregated engine (numpy /
+         OpenBLAS, batch-parallel over host threads) on a bounded sample, rank 0, N=1.
+
+--impl reference times that CPU path alone (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # CPU path parallelises over samples
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "useful GMAC/s per transpose-conv layer and % roofline at 1/2/4/8 B200 vs CPU ref"
+
+# (name, in_h, in_w, c_in, kernel_n, c_out, pad) -- reference GAN_SUITE (bench.py:124-139)
+EBGAN = [("ebgan_l2", 4, 4, 2048, 4, 1024, 2), ("ebgan_l3", 8, 8, 1024, 4, 512, 2),
+         ("ebgan_l4", 16, 16, 512, 4, 256, 2), ("ebgan_l5", 32, 32, 256, 4, 128, 2),
+         ("ebgan_l6", 64, 64, 128, 4, 64, 2), ("ebgan_l7", 128, 128, 64, 4, 64, 2)]
+DCGAN = [("dcgan_l2", 4, 4, 1024, 4, 512, 2), ("dcgan_l3", 8, 8, 512, 4, 256, 2),
+         ("dcgan_l4", 16, 16, 256, 4, 128, 2), ("dcgan_l5", 32, 32, 128, 4, 3, 2)]
+DATASET = [("ds224_k3", 224, 224, 3, 3, 1, 2), ("ds224_k4", 224, 224, 3, 4, 1, 2),
+           ("ds224_k5", 224, 224, 3, 5, 1, 2), ("ds512_k5", 512, 512, 3, 5, 1, 2),
+           ("ds512_k4_c3", 512, 512, 3, 4, 3, 1)]
+MNIST = [("mnist_p0", 28, 28, 1, 3, 1, 0), ("mnist_p1", 28, 28, 1, 3, 1, 1), ("mnist_p2", 28, 28, 1, 3, 1, 2)]
+
+WORKLOADS = {
+    "ebgan_b256_bf16": (EBGAN, 256, "bf16"),
+    "ebgan_b256_fp32": (EBGAN, 256, "fp32"),
+    "dcgan_b256_bf16": (DCGAN, 256, "bf16"),
+    "dcgan_b256_fp32": (DCGAN, 256, "fp32"),
+    "dataset_b64_fp32": (DATASET, 64, "fp32"),
+    "mnist_b64_fp32": (MNIST, 64, "fp32"),
+}
+DEFAULT_WORKLOAD = "ebgan_b256_bf16"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def layer_stats(cfg, batch, dtype):
+    """useful MACs and algorithmic bytes of one layer at `batch`."""
+    name, h, w, ci, n, co, pad = cfg
+    from oracle.segconv_oracle import mult_count_segregated  # noqa: F401 (only for cross-check below)
+    import paper_2502_20493_b200 as P
+    spec = P.TransposeConvSpec(h, w, n, pad, ci, co)
+    macs = P.mult_count_segregated(spec) * batch
+    assert macs == mult_count_segregated(h, w, n, pad, ci, co) * batch
+    e = 2 if dtype == "bf16" else 4
+    oh, ow = P.output_dims(spec)
+    nbytes = batch * ci * h * w * e + batch * co * oh * ow * e + ci * co * n * n * e
+    return macs, nbytes, (oh, ow)
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md "clocks" line)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+
+def cpu_baseline(layers, dtype, budget_s: float = 20.0):
+    """The reference's segregated CPU engine (oracle port: numpy im2col + OpenBLAS GEMM per
+    parity class, engines.py:271-335), batch-parallel over host threads, bounded sample."""
+    from oracle import segconv_oracle as O
+    cores = os.cpu_count() or 1
+    total_macs, total_s, parts = 0, 0.0, []
+    for i, (name, h, w, ci, n, co, pad) in enumerate(layers):
+        in_seed, bank_seed = O.harness_seeds(0, i)
+        bank = O.gen_kernel_bank(ci, co, n, bank_seed)
+        per = O.mult_count_segregated(h, w, n, pad, ci, co)
+        # one warm-up sample, then `cores` samples (at least 1) within the time budget
+        x1 = O.gen_synthetic(ci, h, w, in_seed)
+        t0 = time.perf_counter()
+        O.forward_segregated(x1, bank, pad)
+        one = time.perf_counter() - t0
+        budget_layer = budget_s / len(layers)
+        s = int(max(1, min(cores, 64, budget_layer * cores / max(one, 1e-6))))
+        xs = O.unit_floats(s * ci * h * w, in_seed).reshape(s, ci, h, w)
+        t0 = time.perf_counter()
+        O.forward_segregated_batch(xs, bank, pad, workers=cores)
+        dt = time.perf_counter() - t0
+        total_macs += per * s
+        total_s += dt
+        parts.append(f"{name}:{s}")
+    return {"value": total_macs / total_s / 1e9, "unit": "GMAC/s", "cores": cores, "kind": "port",
+            "sample": f"fp32 numpy/OpenBLAS segregated engine, samples per layer {{{', '.join(parts)}}}, "
+                      f"ThreadPool({cores}) over samples, OPENBLAS_NUM_THREADS=1; per-sample cost is "
+                      f"batch-independent (extrapolated to batch)",
+            "seconds": total_s}
+
+
+def run_reference(args, rank):
+    layers, batch, dtype = WORKLOADS[args.workload]
+    if rank != 0:
+        return 0
+    from oracle import segconv_oracle as O
+    cores = os.cpu_count() or 1
+    s = max(1, min(cores, 16))
+    prepared = []
+    for i, (name, h, w, ci, n, co, pad) in enumerate(layers):
+        in_seed, bank_seed = O.harness_seeds(0, i)
+        prepared.append((O.unit_floats(s * ci * h * w, in_seed).reshape(s, ci, h, w),
+                         O.gen_kernel_bank(ci, co, n, bank_seed), pad,
+                         O.mult_count_segregated(h, w, n, pad, ci, co) * s))
+    macs = sum(p[3] for p in prepared)
+
+    def step():
+        for x, bank, pad, _ in prepared:
+            O.forward_segregated_batch(x, bank, pad, workers=cores)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = macs / dt / 1e9
+    sample = (f"{s} samples per layer per step (bounded sample of batch {batch}), fp32 numpy/OpenBLAS "
+              f"oracle port of the reference segregated engine, ThreadPool({cores}) over samples")
+    out = {"metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference splitmix64 generator)",
+           "config": {"workload": args.workload, "batch_per_gpu": batch, "layers": [c[0] for c in layers]},
+           "impl": "reference",
+           "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": cores, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_20493_b200 as P
+    from paper_2502_20493_b200 import _lib
+    from paper_2502_20493_b200.synth import device_unit_floats, harness_seeds
+
+    layers, batch, dtype = WORKLOADS[args.workload]
+    if args.batch:
+        batch = args.batch
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    stream = torch.cuda.current_stream()
+
+    # --- prepare (untimed, as the reference harness, bench.py:257-258) ---
+    state = []
+    for i, cfg in enumerate(layers):
+        name, h, w, ci, n, co, pad = cfg
+        in_seed, bank_seed = harness_seeds(0, i)
+        bank = device_unit_floats((ci, co, n, n), bank_seed, dtype=torch.float32, device=dev)
+        layer = P.prepare_layer(bank, pad, compute=dtype)
+        # rank r owns samples [r*batch, (r+1)*batch) of the batch stream
+        x = device_unit_floats((batch, ci, h, w), in_seed + rank * batch * ci * h * w, dtype=tdt, device=dev)
+        macs, nbytes, (oh, ow) = layer_stats(cfg, batch, dtype)
+        y = torch.empty((batch, co, oh, ow), dtype=tdt, device=dev)
+        state.append({"name": name, "layer": layer, "x": x, "y": y, "macs": macs, "bytes": nbytes,
+                      "path": layer.select_path(_lib.BF16 if dtype == "bf16" else _lib.F32, batch, h, w),
+                      "flops": 2 * macs})
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        for j, s in enumerate(state):
+            s["layer"].forward(s["x"], out=s["y"])
+            if events is not None:
+                events[j].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    per_layer = [[] for _ in state]
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in state] for _ in range(args.steps)]
+    start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = start.elapsed_time(end) / args.steps
+    for k in range(args.steps):
+        prev = start if k == 0 else evs[k - 1][-1]
+        for j in range(len(state)):
+            per_layer[j].append(prev.elapsed_time(evs[k][j]))
+            prev = evs[k][j]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    peaks = load_peaks()
+    step_macs = sum(s["macs"] for s in state)
+    value = step_macs * world / (ms * 1e-3) / 1e9
+
+    # per-layer roofline (bound = the larger of tensor and HBM time)
+    layer_rows = []
+    for j, s in enumerate(state):
+        lms = float(np.mean(per_layer[j]))
+        t_tensor = s["flops"] / (peaks["bf16_tflops"] * 1e12) if dtype == "bf16" else 0.0
+        t_hbm = s["bytes"] / (peaks["hbm_gbs"] * 1e9)
+        bound = "tensor" if t_tensor > t_hbm else "hbm"
+        if bound == "tensor":
+            achieved, peak, unit = s["flops"] / (lms * 1e-3) / 1e12, peaks["bf16_tflops"], "TFLOP/s"
+        else:
+            achieved, peak, unit = s["bytes"] / (lms * 1e-3) / 1e9, peaks["hbm_gbs"], "GB/s"
+        layer_rows.append({"name": s["name"], "path": s["path"], "ms": lms,
+                           "gmacs": s["macs"] / (lms * 1e-3) / 1e9, "bound": bound,
+                           "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                           "alg_bytes": s["bytes"], "flops": s["flops"]})
+    dom = max(layer_rows, key=lambda r: r["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.workload, {}).get(dom["name"])
+    roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
+                "frac": dom["frac"], "traffic": traffic, "kernel": f"{dom['name']} ({dom['path']})",
+                "share_of_step": dom["ms"] / ms, "peak_source": peaks["source"]}
+
+    # --- e2e through the public API with pinned host buffers ---
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        hx = [s["x"].cpu().pin_memory() for s in state]
+        hy = [torch.empty(s["y"].shape, dtype=tdt).pin_memory() for s in state]
+        h2d = sum(t.numel() * t.element_size() for t in hx)
+        d2h = sum(t.numel() * t.element_size() for t in hy)
+
+        def e2e_step():
+            for s, xi, yi in zip(state, hx, hy):
+                s["layer"].forward(xi, out=yi)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": step_macs * world / (ems * 1e-3) / 1e9, "unit": "GMAC/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems,
+               "steps": e2e_steps, "api": "PreparedLayer.forward(pinned host tensor, out=pinned host tensor)"}
+        del hx, hy
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(layers, dtype, budget_s=args.cpu_budget)
+    total_traffic = sum(s["bytes"] for s in state)
+    out = {"metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16" if dtype == "bf16" else "f32",
+           "data": "synthetic (reference splitmix64 generator, produced on device)",
+           "config": {"workload": args.workload, "batch_per_gpu": batch, "layers": [s["name"] for s in state],
+                      "accumulate": "fp32", "l2": f"inputs larger than L2: {total_traffic / 1e9:.2f} GB "
+                      f"algorithmic traffic per step vs 126 MB L2 (no explicit flush)"},
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+           "clocks": clocks, "layers": layer_rows}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

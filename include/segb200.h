@@ -1,0 +1,134 @@
+/*
+ * segb200 -- C ABI of the B200-native unified kernel-segregated stride-2
+ * transpose convolution (arXiv 2502.20493).
+ *
+ * This is the drop-in boundary for the reference package `segconv`
+ * (/root/reference/pkg/src/segconv). The reference has no FFI; its operator
+ * API is Python. Each entry point below replaces one reference interface,
+ * cited as file:line relative to /root/reference/pkg/src/segconv/. The host
+ * mirror of that Python API (paper_2502_20493_b200/engines.py) binds these
+ * symbols through ctypes; INTEGRATION.md shows the binding a maintainer would
+ * add to the reference itself.
+ *
+ * Conventions
+ *   - plain pointers and sizes; no torch types. Tensor pointers passed to
+ *     segb_prepare / segb_forward / segb_segregate / segb_merge /
+ *     segb_unit_floats are DEVICE pointers owned by the caller.
+ *   - activations are batched NCHW: x (batch, c_in, in_h, in_w),
+ *     y (batch, c_out, out_h, out_w), contiguous. The reference's per-sample
+ *     CHW tensor is batch = 1 (batch is a map over samples).
+ *   - the weight bank is (c_in, c_out, n, n) contiguous, the reference's
+ *     layout (engines.py:213-217), used unflipped in correlation form.
+ *   - every function returns SEGB_OK (0) or an error code; the message is in
+ *     segb_last_error() (thread-local). Codes map to the reference's
+ *     exceptions: SEGB_ERR_SPEC -> SpecError (engines.py:54),
+ *     SEGB_ERR_SHAPE -> ShapeError (tensors.py:26), SEGB_ERR_VALUE ->
+ *     ValueError (engines.py:224-225,251-252), SEGB_ERR_CUDA -> RuntimeError.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream). Launches are
+ *     asynchronous; no function allocates hidden workspace inside forward.
+ *   - results are deterministic: fixed accumulation order, no atomics, no
+ *     split-K, so outputs are bitwise identical across runs and GPU counts.
+ */
+#ifndef SEGB200_H
+#define SEGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEGB_ABI_VERSION 1
+
+enum segb_status {
+    SEGB_OK = 0,
+    SEGB_ERR_SPEC = 1,
+    SEGB_ERR_SHAPE = 2,
+    SEGB_ERR_VALUE = 3,
+    SEGB_ERR_CUDA = 4,
+    SEGB_ERR_UNSUPPORTED = 5
+};
+
+enum segb_dtype { SEGB_F32 = 0, SEGB_F64 = 1, SEGB_BF16 = 2 };
+
+/* engines.py:44-46 ENGINE_REFERENCE / ENGINE_SEGREGATED */
+enum segb_engine { SEGB_ENGINE_REFERENCE = 0, SEGB_ENGINE_SEGREGATED = 1 };
+
+/* kernel selection for segb_forward */
+enum segb_path {
+    SEGB_PATH_AUTO = 0,   /* direct for low-channel layers, igemm where eligible */
+    SEGB_PATH_DIRECT = 1, /* K2: CUDA-core unified kernel, any shape/dtype       */
+    SEGB_PATH_IGEMM = 2   /* K3: tcgen05/TMEM implicit GEMM per parity class     */
+};
+
+typedef struct segb_layer segb_layer;
+
+int segb_abi_version(void);
+const char *segb_last_error(void);
+
+/* engines.py:70-96 (TransposeConvSpec.__post_init__ + output_dims).
+ * SEGB_ERR_SPEC for stride != 2 (not expressible here), in dims < 1,
+ * kernel_n < 2, pad < 0, or an output dim < 1. */
+int segb_output_dims(int in_h, int in_w, int kernel_n, int pad, int *out_h, int *out_w);
+
+/* segregation.py:91-96 effective_padding: pad -> (pad / 2, pad odd).
+ * SEGB_ERR_VALUE for pad < 0 (the reference raises ValueError there). */
+int segb_effective_padding(int pad, int *eff_pad, int *swap);
+
+/* segregation.py:53-58 subkernel_dims */
+int segb_subkernel_dims(int kernel_n, int row_parity, int col_parity, int *rows, int *cols);
+
+/* analysis.py:46-57 mult_count_segregated: useful MACs of one sample.
+ * Returns -1 (and sets the error) on an invalid spec. */
+int64_t segb_mult_count_segregated(int in_h, int in_w, int kernel_n, int pad, int c_in,
+                                   int c_out);
+
+/* K1, segregation.py:61-70 segregate_kernel, batched over `count` kernels:
+ * kern (count, n, n) -> subs = [k00 | k01 | k10 | k11], block (r,s) of shape
+ * (count, R(r), R(s)) with k_rs[u, v] = K[2u + r, 2v + s]. Bit-exact copy.
+ * dtype applies to both arrays (SEGB_F32 / SEGB_F64 / SEGB_BF16). */
+int segb_segregate(const void *kern, int dtype, int64_t count, int kernel_n, void *subs,
+                   void *stream);
+
+/* K1 inverse, segregation.py:73-88 merge_subkernels (same packed layout). */
+int segb_merge(const void *subs, int dtype, int64_t count, int kernel_n, void *kern,
+               void *stream);
+
+/* engines.py:153-160 prepare_layer + engines.py:213-244 PreparedLayer.__init__.
+ * bank: device pointer to (c_in, c_out, n, n) of bank_dtype; copied, so the
+ * caller may free it afterwards. compute_dtype: SEGB_F32 (fp32 FFMA,
+ * the reference's working precision), SEGB_F64 (oracle-grade), SEGB_BF16
+ * (bf16 operands, fp32 accumulation, tensor cores where eligible).
+ * Runs K1 once (the parity split + operand layout), on `stream`. */
+int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int kernel_n, int pad,
+                 int engine, int compute_dtype, void *stream, segb_layer **out);
+
+int segb_layer_info(const segb_layer *layer, int *c_in, int *c_out, int *kernel_n, int *pad,
+                    int *engine, int *compute_dtype);
+
+/* engines.py:246-256 PreparedLayer.forward -> _forward_segregated :271-291.
+ * x: device (batch, c_in, in_h, in_w) of x_dtype; y: device
+ * (batch, c_out, out_h, out_w) of y_dtype, sized by segb_output_dims.
+ * compute_dtype: as segb_prepare, or -1 for the layer's own. Every output
+ * element is written exactly once. */
+int segb_forward(const segb_layer *layer, const void *x, int x_dtype, int64_t batch, int in_h,
+                 int in_w, void *y, int y_dtype, int compute_dtype, int path, void *stream);
+
+/* which kernel SEGB_PATH_AUTO picks for this call (SEGB_PATH_DIRECT/IGEMM) */
+int segb_select_path(const segb_layer *layer, int x_dtype, int64_t batch, int in_h, int in_w,
+                     int compute_dtype);
+
+int segb_release(segb_layer *layer);
+
+/* synth.py:28-39 unit_floats on device: out[i] = float32(float64(
+ * splitmix64(seed + i)) * 2^-64), optionally rounded on to bf16. */
+int segb_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, void *stream);
+
+/* number of kernels this library has launched since load (evidence counter) */
+int64_t segb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEGB200_H */

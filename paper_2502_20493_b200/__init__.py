@@ -1,0 +1,38 @@
+"""B200-native unified kernel-segregated stride-2 transpose convolution.
+
+A drop-in for the segregated-engine path of the reference package `segconv`
+(arXiv 2502.20493): same entry points, padding/output-size conventions and
+error behaviour, with the arithmetic in hand-written sm_100a CUDA kernels
+behind the C ABI of include/segb200.h.
+"""
+
+from .engines import (
+    ENGINE_REFERENCE,
+    ENGINE_SEGREGATED,
+    ENGINES,
+    ComparisonReport,
+    PreparedLayer,
+    compare_outputs,
+    layer_forward,
+    prepare_layer,
+    transpose_conv_reference,
+    transpose_conv_segregated,
+)
+from .errors import ShapeError, SpecError
+from .segregation import SubKernelSet, merge_subkernels, segregate_kernel
+from .spec import (
+    EffectivePadding,
+    TransposeConvSpec,
+    effective_padding,
+    mult_count_segregated,
+    output_dims,
+    subkernel_dims,
+)
+
+__all__ = [
+    "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "EffectivePadding",
+    "PreparedLayer", "ShapeError", "SpecError", "SubKernelSet", "TransposeConvSpec",
+    "compare_outputs", "effective_padding", "layer_forward", "merge_subkernels",
+    "mult_count_segregated", "output_dims", "prepare_layer", "segregate_kernel",
+    "subkernel_dims", "transpose_conv_reference", "transpose_conv_segregated",
+]

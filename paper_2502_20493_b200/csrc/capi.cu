@@ -1,0 +1,297 @@
+// The C ABI (include/segb200.h): validation with the reference's error
+// taxonomy, the prepared-layer object, and kernel dispatch.
+#include <mutex>
+
+#include "common.cuh"
+#include "direct_impl.cuh"
+#include "igemm.cuh"
+#include "kernels.cuh"
+
+namespace segb {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return SEGB_OK;
+}
+
+// engines.py:70-86: TransposeConvSpec.__post_init__ (stride is fixed at 2 here)
+static int check_spec(int in_h, int in_w, int n, int pad, int c_in, int c_out, int *oh, int *ow) {
+    if (in_h < 1 || in_w < 1) return fail(SEGB_ERR_SPEC, "input dims must be >= 1, got %dx%d", in_h, in_w);
+    if (n < 2) return fail(SEGB_ERR_SPEC, "kernel side must be >= 2, got %d", n);
+    if (pad < 0) return fail(SEGB_ERR_SPEC, "padding must be >= 0, got %d", pad);
+    if (c_in < 1 || c_out < 1) return fail(SEGB_ERR_SPEC, "channel counts must be >= 1, got %d->%d", c_in, c_out);
+    const int h = 2 * in_h + 2 * pad - n, w = 2 * in_w + 2 * pad - n;
+    if (h < 1 || w < 1)
+        return fail(SEGB_ERR_SPEC, "output dims %dx%d are not >= 1 (input %dx%d, kernel %d, pad %d)", h, w, in_h,
+                    in_w, n, pad);
+    if (oh) *oh = h;
+    if (ow) *ow = w;
+    return SEGB_OK;
+}
+
+static bool valid_dtype(int dt) { return dt == SEGB_F32 || dt == SEGB_F64 || dt == SEGB_BF16; }
+
+}  // namespace segb
+
+using namespace segb;
+
+struct segb_layer {
+    int c_in, c_out, n, pad, engine, compute;
+    void *bank = nullptr;  // owned device copy of the bank (c_in, c_out, n, n)
+    int bank_dtype;
+    std::mutex mu;
+    void *wd[3] = {nullptr, nullptr, nullptr};  // K2 weights per compute dtype (F32, F64, BF16)
+    int n2p = 0;
+    void *wg = nullptr;  // K3 weights (bf16, class/tap-major, K-major)
+    int c_in_pad = 0;
+};
+
+// K2 weights for a compute dtype, built by K1 on first use (prepare builds the
+// layer's own compute dtype eagerly, so forward only allocates when a caller
+// mixes dtypes, as numpy's result_type promotion in the reference allows).
+static int ensure_direct_weights(segb_layer *L, int compute, cudaStream_t st, const void **out) {
+    std::lock_guard<std::mutex> g(L->mu);
+    if (!L->wd[compute]) {
+        const size_t elt = compute == SEGB_F64 ? 8 : 4;
+        const size_t bytes = elt * (size_t)L->c_out * L->c_in * L->n2p;
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        const int mode = compute == SEGB_F64 ? 1 : (compute == SEGB_BF16 ? 2 : 0);
+        const bool packed = L->engine == SEGB_ENGINE_SEGREGATED;
+        if (int rc = run_prep_direct(L->bank, L->bank_dtype, L->c_in, L->c_out, L->n, L->n2p, packed, mode, p, st)) {
+            cudaFree(p);
+            return rc;
+        }
+        L->wd[compute] = p;
+    }
+    *out = L->wd[compute];
+    return SEGB_OK;
+}
+
+static int ensure_gemm_weights(segb_layer *L, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(L->mu);
+    if (!L->wg) {
+        L->c_in_pad = (int)ceil_div(L->c_in, 64) * 64;
+        const size_t bytes = 2ull * L->n * L->n * L->c_out * L->c_in_pad;
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        if (int rc = run_prep_gemm(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->n, p, st)) {
+            cudaFree(p);
+            return rc;
+        }
+        L->wg = p;
+    }
+    return SEGB_OK;
+}
+
+static bool igemm_ok(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int compute,
+                     int y_dtype) {
+    if (L->engine != SEGB_ENGINE_SEGREGATED || compute != SEGB_BF16) return false;
+    IgemmShape s{};
+    s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
+    s.x_dtype = x_dtype; s.y_dtype = y_dtype;
+    return igemm_supported(s);
+}
+
+extern "C" {
+
+int segb_abi_version(void) { return SEGB_ABI_VERSION; }
+
+const char *segb_last_error(void) { return g_err.c_str(); }
+
+int64_t segb_launch_count(void) { return g_launches.load(); }
+
+int segb_output_dims(int in_h, int in_w, int kernel_n, int pad, int *out_h, int *out_w) {
+    return check_spec(in_h, in_w, kernel_n, pad, 1, 1, out_h, out_w);
+}
+
+int segb_effective_padding(int pad, int *eff_pad, int *swap) {
+    if (pad < 0) return fail(SEGB_ERR_VALUE, "padding must be >= 0, got %d", pad);
+    if (eff_pad) *eff_pad = pad / 2;
+    if (swap) *swap = pad % 2;
+    return SEGB_OK;
+}
+
+int segb_subkernel_dims(int kernel_n, int r, int s, int *rows, int *cols) {
+    if (kernel_n < 2) return fail(SEGB_ERR_SHAPE, "kernel side must be >= 2, got %d", kernel_n);
+    if ((r & ~1) || (s & ~1)) return fail(SEGB_ERR_VALUE, "parities must be 0 or 1, got (%d,%d)", r, s);
+    if (rows) *rows = sub_len(kernel_n, r);
+    if (cols) *cols = sub_len(kernel_n, s);
+    return SEGB_OK;
+}
+
+int64_t segb_mult_count_segregated(int in_h, int in_w, int n, int pad, int c_in, int c_out) {
+    int oh, ow;
+    if (check_spec(in_h, in_w, n, pad, c_in, c_out, &oh, &ow)) return -1;
+    const int swap = pad & 1;
+    int64_t total = 0;
+    for (int r = 0; r < 2; ++r) {
+        const int st_r = (r + swap) % 2;
+        const int64_t rows = std::max(0, (oh - st_r + 1) / 2);
+        for (int s = 0; s < 2; ++s) {
+            const int st_s = (s + swap) % 2;
+            const int64_t cols = std::max(0, (ow - st_s + 1) / 2);
+            total += rows * cols * sub_len(n, r) * sub_len(n, s);
+        }
+    }
+    return total * c_in * c_out;
+}
+
+int segb_segregate(const void *kern, int dtype, int64_t count, int n, void *subs, void *stream) {
+    if (!valid_dtype(dtype)) return fail(SEGB_ERR_VALUE, "unknown dtype %d", dtype);
+    if (n < 2) return fail(SEGB_ERR_SHAPE, "kernel side must be >= 2, got %d", n);
+    if (count < 0 || (count > 0 && (!kern || !subs))) return fail(SEGB_ERR_VALUE, "null tensor");
+    return run_segregate(kern, dtype, count, n, subs, false, (cudaStream_t)stream);
+}
+
+int segb_merge(const void *subs, int dtype, int64_t count, int n, void *kern, void *stream) {
+    if (!valid_dtype(dtype)) return fail(SEGB_ERR_VALUE, "unknown dtype %d", dtype);
+    if (n < 2) return fail(SEGB_ERR_SHAPE, "kernel side must be >= 2, got %d", n);
+    if (count < 0 || (count > 0 && (!kern || !subs))) return fail(SEGB_ERR_VALUE, "null tensor");
+    return run_segregate(subs, dtype, count, n, kern, true, (cudaStream_t)stream);
+}
+
+int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int n, int pad, int engine,
+                 int compute, void *stream, segb_layer **out) {
+    if (!out) return fail(SEGB_ERR_VALUE, "null output handle");
+    *out = nullptr;
+    // engines.py:213-225 validation order: bank shape, kernel side, dtype, pad, engine
+    if (c_in < 1 || c_out < 1) return fail(SEGB_ERR_SHAPE, "kernel bank must have c_in, c_out >= 1");
+    if (n < 2) return fail(SEGB_ERR_SHAPE, "kernel side must be >= 2, got %d", n);
+    if (!valid_dtype(bank_dtype)) return fail(SEGB_ERR_SHAPE, "kernel bank must hold floats (dtype %d)", bank_dtype);
+    if (pad < 0) return fail(SEGB_ERR_SPEC, "padding must be >= 0, got %d", pad);
+    if (engine != SEGB_ENGINE_REFERENCE && engine != SEGB_ENGINE_SEGREGATED)
+        return fail(SEGB_ERR_VALUE, "unknown engine %d, expected one of ('reference', 'segregated')", engine);
+    if (!valid_dtype(compute)) return fail(SEGB_ERR_VALUE, "unknown compute dtype %d", compute);
+    if (!bank) return fail(SEGB_ERR_VALUE, "null bank");
+    cudaStream_t st = (cudaStream_t)stream;
+    segb_layer *L = new segb_layer();
+    L->c_in = c_in; L->c_out = c_out; L->n = n; L->pad = pad; L->engine = engine; L->compute = compute;
+    L->bank_dtype = bank_dtype;
+    L->n2p = (n * n + 3) / 4 * 4;
+    const size_t bytes = dtype_size(bank_dtype) * (size_t)c_in * c_out * n * n;
+    cudaError_t e = cudaMalloc(&L->bank, bytes);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(L->bank, bank, bytes, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+        segb_release(L);
+        return fail(SEGB_ERR_CUDA, "bank copy: %s", cudaGetErrorString(e));
+    }
+    const void *dummy;
+    int rc = ensure_direct_weights(L, compute, st, &dummy);
+    if (!rc && compute == SEGB_BF16 && engine == SEGB_ENGINE_SEGREGATED && igemm_available())
+        rc = ensure_gemm_weights(L, st);
+    if (rc) {
+        segb_release(L);
+        return rc;
+    }
+    *out = L;
+    return SEGB_OK;
+}
+
+int segb_layer_info(const segb_layer *L, int *c_in, int *c_out, int *n, int *pad, int *engine, int *compute) {
+    if (!L) return fail(SEGB_ERR_VALUE, "null layer");
+    if (c_in) *c_in = L->c_in;
+    if (c_out) *c_out = L->c_out;
+    if (n) *n = L->n;
+    if (pad) *pad = L->pad;
+    if (engine) *engine = L->engine;
+    if (compute) *compute = L->compute;
+    return SEGB_OK;
+}
+
+int segb_select_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int compute) {
+    if (!L) return fail(SEGB_ERR_VALUE, "null layer");
+    if (compute < 0) compute = L->compute;
+    return igemm_ok(L, x_dtype, batch, in_h, in_w, compute, SEGB_BF16) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
+}
+
+int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
+                 int y_dtype, int compute, int path, void *stream) {
+    segb_layer *L = const_cast<segb_layer *>(Lc);
+    if (!L) return fail(SEGB_ERR_VALUE, "null layer");
+    if (batch < 1) return fail(SEGB_ERR_SHAPE, "batch must be >= 1, got %lld", (long long)batch);
+    int oh, ow;
+    if (int rc = check_spec(in_h, in_w, L->n, L->pad, L->c_in, L->c_out, &oh, &ow)) return rc;
+    if (!x || !y) return fail(SEGB_ERR_VALUE, "null tensor");
+    if (compute < 0) compute = L->compute;
+    if (!valid_dtype(compute) || !valid_dtype(x_dtype) || !valid_dtype(y_dtype))
+        return fail(SEGB_ERR_VALUE, "unknown dtype (x %d, y %d, compute %d)", x_dtype, y_dtype, compute);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (path == SEGB_PATH_AUTO)
+        path = igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
+    if (path == SEGB_PATH_IGEMM) {
+        if (!igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype))
+            return fail(SEGB_ERR_UNSUPPORTED, "implicit-GEMM path not eligible for this layer/shape/dtype");
+        if (int rc = ensure_gemm_weights(L, st)) return rc;
+        IgemmShape s{};
+        s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
+        s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.c_in_pad = L->c_in_pad;
+        return run_igemm(s, x, L->wg, y, st);
+    }
+    if (path != SEGB_PATH_DIRECT) return fail(SEGB_ERR_VALUE, "unknown path %d", path);
+    const void *w;
+    if (int rc = ensure_direct_weights(L, compute, st, &w)) return rc;
+    DirectArgs a{};
+    a.x = x; a.y = y; a.w = w; a.batch = batch; a.b0 = 0;
+    a.c_in = L->c_in; a.c_out = L->c_out; a.h = in_h; a.w_in = in_w; a.oh = oh; a.ow = ow; a.n = L->n;
+    a.p = L->pad / 2; a.swap = L->pad & 1; a.n2p = L->n2p;
+    a.nqr = (oh - 1 + a.swap) / 2 + 1;
+    a.nqc = (ow - 1 + a.swap) / 2 + 1;
+    const bool ref = L->engine == SEGB_ENGINE_REFERENCE;
+    if (ref) a.p = L->pad;  // the reference engine pads the upsampled map by P
+    switch (compute) {
+        case SEGB_F32:
+            if (x_dtype != SEGB_F32 || y_dtype != SEGB_F32)
+                return fail(SEGB_ERR_VALUE, "fp32 compute needs f32 x and y (got %d/%d)", x_dtype, y_dtype);
+            return launch_direct_f32(a, ref, st);
+        case SEGB_F64:
+            if (x_dtype != SEGB_F64 || y_dtype != SEGB_F64)
+                return fail(SEGB_ERR_VALUE, "fp64 compute needs f64 x and y (got %d/%d)", x_dtype, y_dtype);
+            return launch_direct_f64(a, ref, st);
+        default: return launch_direct_bf16(a, x_dtype, y_dtype, ref, st);
+    }
+}
+
+int segb_release(segb_layer *L) {
+    if (!L) return SEGB_OK;
+    cudaFree(L->bank);
+    for (void *p : L->wd) cudaFree(p);
+    cudaFree(L->wg);
+    delete L;
+    return SEGB_OK;
+}
+
+int segb_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, void *stream) {
+    if (count < 0) return fail(SEGB_ERR_VALUE, "count must be >= 0, got %lld", (long long)count);
+    if (count > 0 && !out) return fail(SEGB_ERR_VALUE, "null tensor");
+    return run_unit_floats(out, dtype, count, seed, (cudaStream_t)stream);
+}
+
+}  // extern "C"

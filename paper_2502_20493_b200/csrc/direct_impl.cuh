@@ -1,0 +1,304 @@
+// K2 -- the direct unified kernel (CUDA cores), templated on element types and
+// the kernel side n.
+//
+// Spec: the per-element unified rule of the reference's instrumented engine,
+// /root/reference/pkg/src/segconv/engines.py:379-406, summed over input
+// channels as engines.py:163-172 (ascending ci, no bias):
+//
+//   r = (x + swap) & 1, s = (y + swap) & 1, p = P/2, swap = P & 1
+//   out[b,co,x,y] = sum_ci sum_{u<R(r), v<R(s)} X[b,ci,(x+r)/2+u-p,(y+s)/2+v-p] * K[ci,co,2u+r,2v+s]
+//
+// One launch covers exactly the output elements; the parity is picked per
+// output by construction (each thread owns whole parity "quads"), the upsampled
+// map is never materialised and the floor(P/2) zero ring is implicit in the
+// predicated loads. Odd output dims compute no stored extra elements.
+//
+// Work decomposition. Let x' = x + swap. A row quad q holds output rows
+// x' in {2q, 2q+1} (r = 0 then r = 1); a column quad t holds y' in {2t, 2t+1}.
+// For quad q, class r = 0 reads input rows q - swap - p + u (u < R0) and
+// class r = 1 reads q + 1 - swap - p + u (u < R1): the union is
+// NW = n/2 + 1 consecutive rows. A thread owns RQ row quads x 1 column quad x
+// COB output channels (2RQ x 2 x COB outputs, all four parity classes), keeps
+// the (RQ + NW - 1) x NW input window of one input channel in registers and
+// reuses each loaded value for every tap and channel that needs it. Lanes of a
+// warp own consecutive column quads, so loads are coalesced row segments and
+// each warp store instruction covers 64 consecutive output columns.
+// Weights (class-packed taps, K1 layout [co][ci][n2p]) are staged in shared
+// memory per 16-input-channel chunk and read as broadcasts.
+#pragma once
+
+#include "common.cuh"
+
+namespace segb {
+
+struct DirectArgs {
+    const void *x;
+    void *y;
+    const void *w;  // [c_out][c_in][n2p] compute type, class-packed taps
+    int64_t batch, b0;  // b0: first sample of this launch (grid z chunking)
+    int c_in, c_out, h, w_in, oh, ow, n, p, swap, n2p;
+    int nqr, nqc;  // row / column quads
+};
+
+constexpr int kDirectCiChunk = 16;
+constexpr int kDirectRowsPerBlock = 4;  // blockDim.y
+
+template <typename TX, typename TC, bool RBF>
+__device__ __forceinline__ TC load_x(const TX *p);
+template <> __device__ __forceinline__ float load_x<float, float, false>(const float *p) { return __ldg(p); }
+template <> __device__ __forceinline__ float load_x<float, float, true>(const float *p) {
+    return round_bf16(__ldg(p));
+}
+template <> __device__ __forceinline__ float load_x<__nv_bfloat16, float, false>(const __nv_bfloat16 *p) {
+    return __bfloat162float(*p);
+}
+template <> __device__ __forceinline__ double load_x<double, double, false>(const double *p) { return __ldg(p); }
+
+template <typename TY, typename TC> __device__ __forceinline__ void store_y(TY *p, TC v);
+template <> __device__ __forceinline__ void store_y<float, float>(float *p, float v) { *p = v; }
+template <> __device__ __forceinline__ void store_y<double, double>(double *p, double v) { *p = v; }
+template <> __device__ __forceinline__ void store_y<__nv_bfloat16, float>(__nv_bfloat16 *p, float v) {
+    *p = __float2bfloat16_rn(v);
+}
+
+template <typename TX, typename TC, typename TY, bool RBF, int N, int COB, int RQ>
+__global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
+    constexpr int NW = N / 2 + 1;
+    constexpr int WR = RQ + NW - 1;
+    constexpr int R0 = (N + 1) / 2, R1 = N / 2;
+    constexpr int OFF1 = R0 * R0, OFF2 = R0 * R0 + R0 * R1, OFF3 = R0 * R0 + 2 * R0 * R1;
+    constexpr int N2 = N * N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TC *ws = reinterpret_cast<TC *>(smem_raw);  // [COB][kDirectCiChunk][n2p]
+
+    const int t = blockIdx.x * 32 + threadIdx.x;
+    const int nrb = (a.nqr + kDirectRowsPerBlock * RQ - 1) / (kDirectRowsPerBlock * RQ);
+    const int q0 = ((blockIdx.y % nrb) * kDirectRowsPerBlock + threadIdx.y) * RQ;
+    const int co0 = (blockIdx.y / nrb) * COB;
+    const int64_t b = a.b0 + blockIdx.z;
+    const int row0 = q0 - a.swap - a.p, col0 = t - a.swap - a.p;
+    const int64_t plane = (int64_t)a.h * a.w_in;
+    const TX *xb = reinterpret_cast<const TX *>(a.x) + b * a.c_in * plane;
+    const TC *wsrc = reinterpret_cast<const TC *>(a.w);
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+
+    TC acc[COB][2 * RQ][2];
+#pragma unroll
+    for (int c = 0; c < COB; ++c)
+#pragma unroll
+        for (int i = 0; i < 2 * RQ; ++i) acc[c][i][0] = acc[c][i][1] = TC(0);
+
+    // per-thread validity of each window row / column (bounds of the input)
+    bool rok[WR], cok[NW];
+#pragma unroll
+    for (int i = 0; i < WR; ++i) rok[i] = (unsigned)(row0 + i) < (unsigned)a.h;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
+
+    for (int ci0 = 0; ci0 < a.c_in; ci0 += kDirectCiChunk) {
+        const int nci = min(kDirectCiChunk, a.c_in - ci0);
+        __syncthreads();
+        for (int i = tid; i < COB * nci * a.n2p; i += 32 * kDirectRowsPerBlock) {
+            const int co = i / (nci * a.n2p);
+            const int rem = i - co * nci * a.n2p;
+            const int ci = rem / a.n2p;
+            const int k = rem - ci * a.n2p;
+            ws[(co * kDirectCiChunk + ci) * a.n2p + k] =
+                (co0 + co < a.c_out) ? wsrc[((int64_t)(co0 + co) * a.c_in + ci0 + ci) * a.n2p + k] : TC(0);
+        }
+        __syncthreads();
+        for (int ci = 0; ci < nci; ++ci) {
+            const TX *xc = xb + (int64_t)(ci0 + ci) * plane;
+            TC win[WR][NW];
+#pragma unroll
+            for (int i = 0; i < WR; ++i)
+#pragma unroll
+                for (int j = 0; j < NW; ++j)
+                    win[i][j] = (rok[i] && cok[j])
+                                    ? load_x<TX, TC, RBF>(xc + (int64_t)(row0 + i) * a.w_in + col0 + j)
+                                    : TC(0);
+#pragma unroll
+            for (int c = 0; c < COB; ++c) {
+                const TC *wp = ws + (c * kDirectCiChunk + ci) * a.n2p;
+                TC wv[N2];
+#pragma unroll
+                for (int k = 0; k < N2; ++k) wv[k] = wp[k];
+#pragma unroll
+                for (int qq = 0; qq < RQ; ++qq) {
+#pragma unroll
+                    for (int u = 0; u < R0; ++u) {
+#pragma unroll
+                        for (int v = 0; v < R0; ++v) acc[c][2 * qq][0] += win[qq + u][v] * wv[u * R0 + v];
+#pragma unroll
+                        for (int v = 0; v < R1; ++v)
+                            acc[c][2 * qq][1] += win[qq + u][1 + v] * wv[OFF1 + u * R1 + v];
+                    }
+#pragma unroll
+                    for (int u = 0; u < R1; ++u) {
+#pragma unroll
+                        for (int v = 0; v < R0; ++v)
+                            acc[c][2 * qq + 1][0] += win[qq + 1 + u][v] * wv[OFF2 + u * R0 + v];
+#pragma unroll
+                        for (int v = 0; v < R1; ++v)
+                            acc[c][2 * qq + 1][1] += win[qq + 1 + u][1 + v] * wv[OFF3 + u * R1 + v];
+                    }
+                }
+            }
+        }
+    }
+
+    // stores: each output written exactly once; the quad positions outside
+    // [0, oh) x [0, ow) (odd dims, the swap shift) are not stored
+    TY *yb = reinterpret_cast<TY *>(a.y);
+    const int y_first = 2 * t - a.swap;
+#pragma unroll
+    for (int c = 0; c < COB; ++c) {
+        if (co0 + c >= a.c_out) break;
+        TY *yc = yb + ((int64_t)b * a.c_out + co0 + c) * a.oh * a.ow;
+#pragma unroll
+        for (int i = 0; i < 2 * RQ; ++i) {
+            const int xo = 2 * q0 + i - a.swap;
+            if ((unsigned)xo >= (unsigned)a.oh) continue;
+            TY *row = yc + (int64_t)xo * a.ow;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const int yo = y_first + s;
+                if ((unsigned)yo < (unsigned)a.ow) store_y<TY, TC>(row + yo, acc[c][i][s]);
+            }
+        }
+    }
+}
+
+// Generic-n fallback (n > 9): one thread per output element, runtime loops.
+template <typename TX, typename TC, typename TY, bool RBF>
+__global__ void __launch_bounds__(256) direct_generic_kernel(DirectArgs a) {
+    const int64_t total = a.batch * a.c_out * (int64_t)a.oh * a.ow;
+    const int64_t plane = (int64_t)a.h * a.w_in;
+    const TC *wsrc = reinterpret_cast<const TC *>(a.w);
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int yo = idx % a.ow;
+        const int xo = (idx / a.ow) % a.oh;
+        const int co = (idx / ((int64_t)a.ow * a.oh)) % a.c_out;
+        const int64_t b = idx / ((int64_t)a.ow * a.oh * a.c_out);
+        const int r = (xo + a.swap) & 1, s = (yo + a.swap) & 1;
+        const int bx = (xo + r) / 2 - a.p, by = (yo + s) / 2 - a.p;
+        const int R = sub_len(a.n, r), C = sub_len(a.n, s), off = class_offset(a.n, 2 * r + s);
+        TC acc = 0;
+        for (int ci = 0; ci < a.c_in; ++ci) {
+            const TX *xc = reinterpret_cast<const TX *>(a.x) + (b * a.c_in + ci) * plane;
+            const TC *wp = wsrc + ((int64_t)co * a.c_in + ci) * a.n2p + off;
+            for (int u = 0; u < R; ++u) {
+                const int ii = bx + u;
+                if ((unsigned)ii >= (unsigned)a.h) continue;
+                for (int v = 0; v < C; ++v) {
+                    const int jj = by + v;
+                    if ((unsigned)jj >= (unsigned)a.w_in) continue;
+                    acc += load_x<TX, TC, RBF>(xc + (int64_t)ii * a.w_in + jj) * wp[u * C + v];
+                }
+            }
+        }
+        store_y<TY, TC>(reinterpret_cast<TY *>(a.y) + idx, acc);
+    }
+}
+
+// The reference engine (Alg. 1, engines.py:134-140 / 258-269) on the device:
+// correlation of the zero-padded bed-of-nails map with the full n x n kernel,
+// evaluated without materialising the map (zero taps are still multiplied, as
+// the reference does). Weights: the raw bank in compute type, [co][ci][n*n].
+template <typename TX, typename TC, typename TY, bool RBF>
+__global__ void __launch_bounds__(256) reference_engine_kernel(DirectArgs a, int pad) {
+    const int64_t total = a.batch * a.c_out * (int64_t)a.oh * a.ow;
+    const int64_t plane = (int64_t)a.h * a.w_in;
+    const TC *wsrc = reinterpret_cast<const TC *>(a.w);
+    const int n = a.n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int yo = idx % a.ow;
+        const int xo = (idx / a.ow) % a.oh;
+        const int co = (idx / ((int64_t)a.ow * a.oh)) % a.c_out;
+        const int64_t b = idx / ((int64_t)a.ow * a.oh * a.c_out);
+        TC acc = 0;
+        for (int ci = 0; ci < a.c_in; ++ci) {
+            const TX *xc = reinterpret_cast<const TX *>(a.x) + (b * a.c_in + ci) * plane;
+            const TC *wp = wsrc + ((int64_t)co * a.c_in + ci) * a.n2p;
+            for (int u = 0; u < n; ++u) {
+                const int uu = xo + u - pad;  // index into the un-padded upsampled map
+                const bool rlive = uu >= 0 && (uu & 1) == 0 && (uu >> 1) < a.h;
+                for (int v = 0; v < n; ++v) {
+                    const int vv = yo + v - pad;
+                    const bool live = rlive && vv >= 0 && (vv & 1) == 0 && (vv >> 1) < a.w_in;
+                    const TC val = live ? load_x<TX, TC, RBF>(xc + (int64_t)(uu >> 1) * a.w_in + (vv >> 1)) : TC(0);
+                    acc += val * wp[u * n + v];
+                }
+            }
+        }
+        store_y<TY, TC>(reinterpret_cast<TY *>(a.y) + idx, acc);
+    }
+}
+
+template <typename TX, typename TC, typename TY, bool RBF, int N, int COB>
+int launch_direct_n(const DirectArgs &a, cudaStream_t st) {
+    constexpr int RQ = (N <= 5) ? 4 : 2;
+    dim3 block(32, kDirectRowsPerBlock);
+    const int64_t nco_blk = ceil_div(a.c_out, COB);
+    const int64_t nrb = ceil_div(a.nqr, kDirectRowsPerBlock * RQ);
+    if (nco_blk * nrb > 65535 || ceil_div(a.nqc, 32) > (1ll << 31) - 1)
+        return fail(SEGB_ERR_UNSUPPORTED, "output too large for the direct kernel grid");
+    const size_t smem = sizeof(TC) * COB * kDirectCiChunk * a.n2p;
+    for (int64_t b0 = 0; b0 < a.batch; b0 += 65535) {
+        DirectArgs c = a;
+        c.b0 = b0;
+        dim3 grid((unsigned)ceil_div(a.nqc, 32), (unsigned)(nco_blk * nrb),
+                  (unsigned)std::min<int64_t>(65535, a.batch - b0));
+        direct_kernel<TX, TC, TY, RBF, N, COB, RQ><<<grid, block, smem, st>>>(c);
+        note_launch();
+        if (int rc = check_launch("direct_kernel")) return rc;
+    }
+    return SEGB_OK;
+}
+
+template <typename TX, typename TC, typename TY, bool RBF, int N>
+int launch_direct_cob(const DirectArgs &a, cudaStream_t st) {
+    if (a.c_out == 1) return launch_direct_n<TX, TC, TY, RBF, N, 1>(a, st);
+    if (a.c_out == 2) return launch_direct_n<TX, TC, TY, RBF, N, 2>(a, st);
+    if (a.c_out == 3) return launch_direct_n<TX, TC, TY, RBF, N, 3>(a, st);
+    return launch_direct_n<TX, TC, TY, RBF, N, 4>(a, st);
+}
+
+template <typename TX, typename TC, typename TY, bool RBF>
+int launch_direct_typed(const DirectArgs &a, bool reference_engine, cudaStream_t st) {
+    const int64_t total = a.batch * a.c_out * (int64_t)a.oh * a.ow;
+    if (reference_engine) {
+        const int threads = 256;
+        const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), 148 * 64);
+        reference_engine_kernel<TX, TC, TY, RBF><<<(unsigned)blocks, threads, 0, st>>>(a, a.p);
+        note_launch();
+        return check_launch("reference_engine_kernel");
+    }
+    switch (a.n) {
+        case 2: return launch_direct_cob<TX, TC, TY, RBF, 2>(a, st);
+        case 3: return launch_direct_cob<TX, TC, TY, RBF, 3>(a, st);
+        case 4: return launch_direct_cob<TX, TC, TY, RBF, 4>(a, st);
+        case 5: return launch_direct_cob<TX, TC, TY, RBF, 5>(a, st);
+        case 6: return launch_direct_cob<TX, TC, TY, RBF, 6>(a, st);
+        case 7: return launch_direct_cob<TX, TC, TY, RBF, 7>(a, st);
+        case 8: return launch_direct_cob<TX, TC, TY, RBF, 8>(a, st);
+        case 9: return launch_direct_cob<TX, TC, TY, RBF, 9>(a, st);
+        default: {
+            const int threads = 256;
+            const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), 148 * 64);
+            direct_generic_kernel<TX, TC, TY, RBF><<<(unsigned)blocks, threads, 0, st>>>(a);
+            note_launch();
+            return check_launch("direct_generic_kernel");
+        }
+    }
+}
+
+// per-dtype-combination entry points (defined in direct_*.cu)
+int launch_direct_f32(const DirectArgs &a, bool ref_engine, cudaStream_t st);
+int launch_direct_f64(const DirectArgs &a, bool ref_engine, cudaStream_t st);
+// bf16 compute: x in {f32 (rounded on load), bf16}, y in {f32, bf16}
+int launch_direct_bf16(const DirectArgs &a, int x_dtype, int y_dtype, bool ref_engine, cudaStream_t st);
+
+}  // namespace segb

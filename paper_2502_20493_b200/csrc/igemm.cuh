@@ -1,0 +1,17 @@
+// K3 interface: per-parity-class implicit GEMM on tcgen05/TMEM (igemm_sm100.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace segb {
+
+struct IgemmShape {
+    int64_t batch;
+    int c_in, c_out, h, w, n, pad, x_dtype, y_dtype, c_in_pad;
+};
+
+bool igemm_available();
+bool igemm_supported(const IgemmShape &s);
+int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st);
+
+}  // namespace segb

@@ -1,0 +1,310 @@
+"""Drop-in operator API of the segregated transpose convolution, on the B200.
+
+Mirrors /root/reference/pkg/src/segconv/engines.py -- same names, argument
+meaning and error behaviour -- with the arithmetic on the GPU through the
+C ABI (include/segb200.h):
+
+  prepare_layer / PreparedLayer.__init__   engines.py:153-160, 213-244  -> segb_prepare (K1)
+  PreparedLayer.forward                    engines.py:246-256, 271-291  -> segb_forward (K2 / K3)
+  layer_forward                            engines.py:163-172
+  transpose_conv_segregated                engines.py:143-150
+  transpose_conv_reference (Alg. 1)        engines.py:134-140 (the GPU reference engine)
+  compare_outputs / ComparisonReport       engines.py:99-118, 175-198 (host-side verdict)
+
+Extensions over the reference (documented in DESIGN.md): forward also takes
+torch tensors, CUDA-resident (C,H,W) or batched (B,C,H,W), returning a torch
+tensor on the same device (or writing into `out=`); a CPU torch tensor (e.g.
+pinned) is copied in and the result copied back; `compute="bf16"` selects
+bf16 operands with fp32 accumulation (tensor cores where eligible).
+There is no CPU fallback: without the CUDA library or a GPU these raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device, _lib
+from .errors import ShapeError, SpecError
+from .segregation import SubKernelSet, merge_subkernels, require_square_kernel
+from .spec import TransposeConvSpec, output_dims, _spec_dims
+
+ENGINE_REFERENCE = "reference"
+ENGINE_SEGREGATED = "segregated"
+ENGINES = (ENGINE_REFERENCE, ENGINE_SEGREGATED)
+
+COMPUTE_DTYPES = {"fp32": _lib.F32, "fp64": _lib.F64, "bf16": _lib.BF16}
+
+
+@dataclass(frozen=True)
+class ComparisonReport:
+    """Element-wise agreement between two tensors (the second one is the reference)."""
+
+    shapes_match: bool
+    max_abs_diff: float | None
+    max_rel_diff: float | None
+    rel_tol: float
+    abs_tol: float
+    passed: bool
+
+    def to_dict(self) -> dict:
+        return {"shapes_match": self.shapes_match, "max_abs_diff": self.max_abs_diff,
+                "max_rel_diff": self.max_rel_diff, "rel_tol": self.rel_tol,
+                "abs_tol": self.abs_tol, "passed": self.passed}
+
+
+def compare_outputs(a, b, rel_tol: float = 1e-5, abs_tol: float = 1e-6) -> ComparisonReport:
+    """engines.py:175-198: pass iff |a - b| <= abs_tol + rel_tol * |b| everywhere."""
+    a = _as_numpy(a)
+    b = _as_numpy(b)
+    if a.shape != b.shape:
+        return ComparisonReport(False, None, None, rel_tol, abs_tol, False)
+    a64 = a.astype(np.float64, copy=False)
+    b64 = b.astype(np.float64, copy=False)
+    d = np.abs(a64 - b64)
+    den = np.maximum(np.abs(a64), np.abs(b64))
+    rel = np.divide(d, den, out=np.zeros_like(d), where=den > 0)
+    passed = bool(np.all(d <= abs_tol + rel_tol * np.abs(b64)))
+    return ComparisonReport(True, float(d.max()) if d.size else 0.0,
+                            float(rel.max()) if rel.size else 0.0, rel_tol, abs_tol, passed)
+
+
+def _as_numpy(a):
+    if isinstance(a, np.ndarray):
+        return a
+    mod = type(a).__module__
+    if mod.startswith("torch"):
+        return a.detach().float().cpu().numpy() if a.dtype == _device.torch().bfloat16 \
+            else a.detach().cpu().numpy()
+    return np.asarray(a)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def require_channel_tensor(arr, what: str = "channel tensor"):
+    """tensors.py:52-60 (numpy), extended to torch (C,H,W) / (B,C,H,W)."""
+    if _is_torch(arr):
+        t = _device.torch()
+        if arr.dim() not in (3, 4):
+            raise ShapeError(f"{what} must be a 3-D (channels, height, width) or 4-D batched "
+                             f"tensor, got {tuple(arr.shape)}")
+        if min(arr.shape) < 1:
+            raise ShapeError(f"{what} dimensions must all be >= 1, got {tuple(arr.shape)}")
+        if arr.dtype not in (t.float32, t.float64, t.bfloat16):
+            raise ShapeError(f"{what} must hold floats, got dtype {arr.dtype}")
+        return arr
+    if not isinstance(arr, np.ndarray) or arr.ndim != 3:
+        raise ShapeError(f"{what} must be a 3-D (channels, height, width) array, "
+                         f"got {getattr(arr, 'shape', type(arr))}")
+    if min(arr.shape) < 1:
+        raise ShapeError(f"{what} dimensions must all be >= 1, got {arr.shape}")
+    if not np.issubdtype(arr.dtype, np.floating):
+        raise ShapeError(f"{what} must hold floats, got dtype {arr.dtype}")
+    return arr
+
+
+class PreparedLayer:
+    """A kernel bank laid out on the device for one engine (engines.py:204-244).
+
+    Construction validates like the reference, uploads the (c_in, c_out, n, n)
+    bank and runs K1 (segb_prepare): the parity split into the four class
+    sub-banks, in the operand layout of the kernel that will consume them.
+    Immutable afterwards and safe to share across threads and streams.
+    """
+
+    def __init__(self, bank, pad: int, engine: str = ENGINE_SEGREGATED, compute: str | None = None):
+        t = _device.torch()
+        is_t = _is_torch(bank)
+        shape = tuple(bank.shape)
+        if len(shape) != 4 or shape[2] != shape[3]:
+            raise ShapeError(f"kernel bank must be (c_in, c_out, n, n) with square "
+                             f"kernels, got shape {shape}")
+        if shape[2] < 2:
+            raise ShapeError(f"kernel side must be >= 2, got {shape[2]}")
+        if is_t:
+            if bank.dtype not in (t.float32, t.float64, t.bfloat16):
+                raise ShapeError(f"kernel bank must hold floats, got dtype {bank.dtype}")
+        else:
+            bank = np.asarray(bank)
+            if not np.issubdtype(bank.dtype, np.floating):
+                raise ShapeError(f"kernel bank must hold floats, got dtype {bank.dtype}")
+        if pad < 0:
+            raise SpecError(f"padding must be >= 0, got {pad}")
+        if engine not in ENGINES:
+            raise ValueError(f"unknown engine {engine!r}, expected one of {ENGINES}")
+        self.engine = engine
+        self.pad = int(pad)
+        self.c_in, self.c_out, self.kernel_n = shape[0], shape[1], shape[2]
+        if is_t:
+            self.bank_dtype = {t.float32: np.float32, t.float64: np.float64}.get(bank.dtype, np.float32)
+        else:
+            self.bank_dtype = bank.dtype
+        if compute is None:
+            compute = "fp64" if self.bank_dtype == np.float64 else "fp32"
+        if compute not in COMPUTE_DTYPES:
+            raise ValueError(f"unknown compute dtype {compute!r}, expected one of {tuple(COMPUTE_DTYPES)}")
+        self.compute = compute
+        _device.require_cuda()
+        if is_t:
+            d_bank = bank.detach().contiguous()
+            if not d_bank.is_cuda:
+                d_bank = d_bank.to(t.cuda.current_device())
+        else:
+            work = bank if bank.dtype in (np.float32, np.float64) else bank.astype(np.float64)
+            d_bank = _device.to_device(work)
+        self.device = d_bank.device
+        handle = ctypes.c_void_p()
+        _lib.check(_lib.lib().segb_prepare(
+            d_bank.data_ptr(), _device.dtype_id(d_bank.dtype), self.c_in, self.c_out, self.kernel_n,
+            self.pad, _lib.ENGINE_IDS[engine], COMPUTE_DTYPES[compute], _device.stream_ptr(self.device),
+            ctypes.byref(handle)))
+        self._handle = handle
+        self._lib = _lib.lib()
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.segb_release(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._handle = None
+
+    # ------------------------------------------------------------------
+    def output_shape(self, in_h: int, in_w: int) -> tuple[int, int]:
+        return _spec_dims(in_h, in_w, self.kernel_n, self.pad)
+
+    def select_path(self, x_dtype_id: int, batch: int, in_h: int, in_w: int,
+                    compute: str | None = None) -> str:
+        cid = COMPUTE_DTYPES[compute or self.compute]
+        p = self._lib.segb_select_path(self._handle, x_dtype_id, batch, in_h, in_w, cid)
+        return {1: "direct", 2: "igemm"}[p]
+
+    def forward(self, x, threads: int = 1, out=None, path: str = "auto", out_dtype=None):
+        """engines.py:246-256. numpy (C,H,W) in -> numpy out (dtype = result_type of
+        x and bank, as the reference); torch in -> torch out."""
+        x = require_channel_tensor(x)
+        c_axis = 1 if (_is_torch(x) and x.dim() == 4) else 0
+        if x.shape[c_axis] != self.c_in:
+            raise ShapeError(f"channel mismatch: input has {x.shape[c_axis]} channels, "
+                             f"bank expects {self.c_in}")
+        if threads < 1:
+            raise ValueError(f"threads must be >= 1, got {threads}")
+        in_h, in_w = int(x.shape[-2]), int(x.shape[-1])
+        out_h, out_w = self.output_shape(in_h, in_w)
+        if path not in _lib.PATH_IDS:
+            raise ValueError(f"unknown path {path!r}, expected one of {tuple(_lib.PATH_IDS)}")
+        if _is_torch(x):
+            return self._forward_torch(x, out, path, out_dtype, out_h, out_w)
+        return self._forward_numpy(x, out_h, out_w, path)
+
+    def _compute_for(self, x_dt) -> str:
+        if self.compute == "bf16":
+            return "bf16"
+        t = _device.torch()
+        if x_dt in (np.float64, t.float64) or self.bank_dtype == np.float64:
+            return "fp64"
+        return "fp32"
+
+    def _forward_numpy(self, x: np.ndarray, out_h: int, out_w: int, path: str) -> np.ndarray:
+        t = _device.torch()
+        dt = np.result_type(x.dtype, self.bank_dtype)
+        compute = self._compute_for(np.float64 if dt == np.float64 else np.float32)
+        host_dt = np.float64 if compute == "fp64" else np.float32
+        d_x = _device.to_device(x.astype(host_dt, copy=False)[None], self.device)
+        d_y = t.empty((1, self.c_out, out_h, out_w), dtype=_device.torch_dtype(_device.dtype_id(host_dt)),
+                      device=self.device)
+        self._launch(d_x, d_y, compute, path)
+        return d_y[0].cpu().numpy().astype(dt, copy=False)
+
+    def _forward_torch(self, x, out, path, out_dtype, out_h, out_w):
+        t = _device.torch()
+        squeeze = x.dim() == 3
+        xb = x[None] if squeeze else x
+        host_in = not xb.is_cuda
+        if host_in:
+            xb = xb.to(self.device, non_blocking=True)
+        elif xb.device != self.device:
+            raise ValueError(f"input on {xb.device}, layer prepared on {self.device}")
+        xb = xb.contiguous()
+        compute = self._compute_for(xb.dtype)
+        if compute == "fp64" and xb.dtype != t.float64:
+            xb = xb.double()
+        if compute == "fp32" and xb.dtype != t.float32:
+            xb = xb.float()
+        if out_dtype is None:
+            out_dtype = (out.dtype if out is not None else
+                         (t.bfloat16 if compute == "bf16" and xb.dtype == t.bfloat16 else
+                          (t.float64 if compute == "fp64" else t.float32)))
+        shape = (xb.shape[0], self.c_out, out_h, out_w)
+        if out is not None and out.is_cuda:
+            if tuple(out.shape) not in (shape, shape[1:] if squeeze else shape) or not out.is_contiguous():
+                raise ShapeError(f"out must be a contiguous {shape} tensor, got {tuple(out.shape)}")
+            if out.dtype != out_dtype:
+                raise ValueError(f"out dtype {out.dtype} != {out_dtype}")
+            d_y = out.view(shape)
+        else:
+            d_y = t.empty(shape, dtype=out_dtype, device=self.device)
+        self._launch(xb, d_y, compute, path)
+        if out is not None and not out.is_cuda:
+            out.view(shape).copy_(d_y, non_blocking=True)
+            return out
+        if host_in:
+            return (d_y[0] if squeeze else d_y).to("cpu")
+        return d_y[0] if squeeze else d_y
+
+    def _launch(self, d_x, d_y, compute: str, path: str) -> None:
+        b, _, h, w = d_x.shape
+        _lib.check(self._lib.segb_forward(
+            self._handle, d_x.data_ptr(), _device.dtype_id(d_x.dtype), int(b), int(h), int(w),
+            d_y.data_ptr(), _device.dtype_id(d_y.dtype), COMPUTE_DTYPES[compute],
+            _lib.PATH_IDS[path], _device.stream_ptr(self.device)))
+
+
+def prepare_layer(bank, pad: int, engine: str = ENGINE_SEGREGATED, compute: str | None = None) -> PreparedLayer:
+    """engines.py:153-160: lay out a (c_in, c_out, n, n) bank once for repeated forwards."""
+    return PreparedLayer(bank, pad, engine, compute)
+
+
+def layer_forward(x, bank, pad: int, engine: str = ENGINE_SEGREGATED, threads: int = 1,
+                  compute: str | None = None):
+    """engines.py:163-172: out[co] = sum_ci tconv(x[ci], bank[ci, co], pad)."""
+    return prepare_layer(bank, pad, engine, compute).forward(x, threads=threads)
+
+
+def require_feature_map(arr, what: str = "feature map") -> np.ndarray:
+    """tensors.py:42-49."""
+    if not isinstance(arr, np.ndarray) or arr.ndim != 2:
+        raise ShapeError(f"{what} must be a 2-D array, got {getattr(arr, 'shape', type(arr))}")
+    if arr.shape[0] < 1 or arr.shape[1] < 1:
+        raise ShapeError(f"{what} must be at least 1x1, got {arr.shape}")
+    if not np.issubdtype(arr.dtype, np.floating):
+        raise ShapeError(f"{what} must hold floats, got dtype {arr.dtype}")
+    return arr
+
+
+def transpose_conv_segregated(feature_map, subs: SubKernelSet, pad: int) -> np.ndarray:
+    """engines.py:143-150: single map through merge -> prepare -> forward."""
+    m = require_feature_map(feature_map)
+    _spec_dims(m.shape[0], m.shape[1], subs.size, pad)
+    bank = merge_subkernels(subs)[np.newaxis, np.newaxis]
+    return prepare_layer(bank, pad, ENGINE_SEGREGATED).forward(m[np.newaxis])[0]
+
+
+def transpose_conv_reference(feature_map, kernel, pad: int) -> np.ndarray:
+    """engines.py:134-140: Alg. 1 (upsample -> pad P -> correlate), evaluated on the GPU."""
+    m = require_feature_map(feature_map)
+    k = require_square_kernel(kernel)
+    _spec_dims(m.shape[0], m.shape[1], k.shape[0], pad)
+    return prepare_layer(k[np.newaxis, np.newaxis], pad, ENGINE_REFERENCE).forward(m[np.newaxis])[0]
+
+
+__all__ = [
+    "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "PreparedLayer",
+    "SpecError", "ShapeError", "TransposeConvSpec", "compare_outputs", "layer_forward",
+    "output_dims", "prepare_layer", "transpose_conv_reference", "transpose_conv_segregated",
+]
