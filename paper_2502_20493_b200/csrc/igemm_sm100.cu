@@ -1,10 +1,454 @@
-// K3 placeholder (filled in by the tcgen05 implementation).
+// K3 -- per-parity-class implicit GEMM on the 5th-gen tensor cores (sm_100a).
+//
+// For parity class (r, s) of the unified rule (engines.py:271-291 computes the
+// same per-class product with an explicit im2col + BLAS GEMM, :309-335):
+//
+//   out[b, co, 2i + st_r, 2j + st_s] = sum_{u<R(r), v<R(s), ci}
+//        X[b, ci, i + base_r + u - p, j + base_s + v - p] * K[ci, co, 2u + r, 2v + s]
+//
+// i.e. a GEMM with M = positions (b, i, j) of the class grid, N = c_out,
+// K = (tap (u, v), ci). Nothing is materialised: the A operand of tap (u, v)
+// is a TMA box of the channels-last activations at coordinates shifted by the
+// tap, and TMA's out-of-bounds zero fill *is* the floor(P/2) zero ring.
+//
+// Kernel: persistent, warp-specialised, one CTA per SM.
+//   warp 0      TMA producer  (A box + B tile per k-step into a 4..8-stage ring)
+//   warp 1      MMA issuer    (tcgen05.mma.cta_group::1.kind::f16, M=128, N=n_tile,
+//                              fp32 accumulators in TMEM, double-buffered)
+//   warps 2..5  epilogue      (tcgen05.ld -> registers -> NCHW stores of the class
+//                              positions; each output element written once)
+// Operands: A = activations NHWC bf16 (K-major, SWIZZLE_128B, 64 channels =
+// 128 B per row), B = K1-prepared weights [tap][c_out][c_in_pad] bf16 (K-major,
+// SWIZZLE_128B). Tiles: (class, 128 positions, n_tile output channels); the
+// class index varies fastest so the four parity classes of a position block run
+// concurrently on neighbouring SMs (shared input windows hit in L2, and their
+// interleaved stride-2 output sectors are completed in L2 before write-back).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "igemm.cuh"
 
 namespace segb {
-bool igemm_available() { return false; }
-bool igemm_supported(const IgemmShape &) { return false; }
-int run_igemm(const IgemmShape &, const void *, const void *, void *, cudaStream_t) {
-    return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM not built");
+
+constexpr int kThreads = 192;
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 64;  // channels per k-step (128 B of bf16)
+
+struct ClassGeom {
+    int R, C;             // sub-kernel rows / cols
+    int rows, cols;       // class grid
+    int st_r, st_s;       // first output row / col of the class
+    int base_r, base_s;   // first window base (engines.py:338-347)
+    int tap0;             // class-packed tap index of (u, v) = (0, 0)
+};
+
+struct IgemmParams {
+    ClassGeom cls[4];
+    int batch, c_in, c_out, oh, ow, p;
+    int n_tile, n_blocks, k_cblocks, m_tiles, total_tiles, stages;
+    int box_w, box_h, box_b;  // A box (positions): cols x rows x samples = 128
+    int64_t class_positions;  // batch * rows * cols (identical for all classes here)
+    void *y;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 32 lanes x 32 consecutive fp32 columns; thread t of the warp gets lane (quarter*32 + t)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor (sm100 "version 1"): K-major, SWIZZLE_128B,
+// 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(16 >> 4) << 16;    // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset: 8 rows x 128 B
+    d |= 1ull << 46;                   // descriptor version (sm100)
+    d |= 2ull << 61;                   // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: bf16 x bf16 -> fp32, A and B K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBlockM >> 4) << 24);
+}
+
+template <typename TY> __device__ __forceinline__ TY cvt_out(float v);
+template <> __device__ __forceinline__ float cvt_out<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// ---------------------------------------------------------------- the kernel
+template <typename TY>
+__global__ void __launch_bounds__(kThreads, 1)
+    igemm_tconv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const IgemmParams prm) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for SWIZZLE_128B atoms
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = prm.stages;
+    const uint32_t a_bytes = kBlockM * kBlockK * 2;
+    const uint32_t b_bytes = prm.n_tile * kBlockK * 2;
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + S * a_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * b_bytes);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int N = prm.n_tile;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 1) {  // TMEM: two accumulator buffers of N fp32 columns
+        const uint32_t cols = 2 * N < 32 ? 32 : 2 * N;
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int S_ = S;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
+                const int c = t & 3, rest = t >> 2;
+                const int mb = rest % prm.m_tiles, nb = rest / prm.m_tiles;
+                const ClassGeom &g = prm.cls[c];
+                const int64_t P0 = (int64_t)mb * kBlockM;
+                const int64_t per = (int64_t)g.rows * g.cols;
+                const int b0 = (int)(P0 / per);
+                const int rem = (int)(P0 - b0 * per);
+                const int i0 = rem / g.cols, j0 = rem % g.cols;
+                for (int u = 0; u < g.R; ++u)
+                    for (int v = 0; v < g.C; ++v)
+                        for (int kb = 0; kb < prm.k_cblocks; ++kb) {
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            mbar_expect_tx(&full[stage], a_bytes + b_bytes);
+                            tma_load_4d(sA + stage * a_bytes, &tmA, &full[stage], kb * kBlockK,
+                                        j0 + g.base_s + v - prm.p, i0 + g.base_r + u - prm.p, b0);
+                            tma_load_3d(sB + stage * b_bytes, &tmB, &full[stage], kb * kBlockK, nb * N,
+                                        g.tap0 + u * g.C + v);
+                            if (++stage == S_) { stage = 0; phase ^= 1; }
+                        }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            const uint32_t idesc = idesc_bf16(N);
+            for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
+                const ClassGeom &g = prm.cls[t & 3];
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * N;
+                const int ksteps = g.R * g.C * prm.k_cblocks;
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * a_bytes), b0 = smem_u32(sB + stage * b_bytes);
+#pragma unroll
+                    for (int kk = 0; kk < kBlockK / 16; ++kk)
+                        tc_mma(d, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, (ks | kk) != 0);
+                    tc_commit(&empty[stage]);
+                    if (++stage == S_) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {  // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int64_t plane = (int64_t)prm.oh * prm.ow;
+        TY *y = reinterpret_cast<TY *>(prm.y);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
+            const int c = t & 3, rest = t >> 2;
+            const int mb = rest % prm.m_tiles, nb = rest / prm.m_tiles;
+            const ClassGeom &g = prm.cls[c];
+            const int64_t pos = (int64_t)mb * kBlockM + m;
+            const bool valid = pos < prm.class_positions;
+            const int64_t per = (int64_t)g.rows * g.cols;
+            const int64_t b = pos / per;
+            const int rem = (int)(pos - b * per);
+            const int x = 2 * (rem / g.cols) + g.st_r, yy = 2 * (rem % g.cols) + g.st_s;
+            TY *dst = y + (b * prm.c_out + (int64_t)nb * N) * plane + (int64_t)x * prm.ow + yy;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            for (int ch = 0; ch < N / 32; ++ch) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * N + ch * 32, v);
+                if (valid) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) dst[(int64_t)(ch * 32 + k) * plane] = cvt_out<TY>(__uint_as_float(v[k]));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        const uint32_t cols = 2 * N < 32 ? 32 : 2 * N;
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
+    }
+}
+
+// NCHW (bf16 or fp32) -> NHWC bf16 staging: the channels-last A operand.
+template <typename TX>
+__global__ void nchw_to_nhwc_bf16(const TX *__restrict__ x, __nv_bfloat16 *__restrict__ y, int C, int HW) {
+    __shared__ float tile[32][33];
+    const int64_t b = blockIdx.z;
+    const int hw0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const TX *xb = x + b * C * (int64_t)HW;
+    __nv_bfloat16 *yb = y + b * C * (int64_t)HW;
+    for (int k = threadIdx.y; k < 32; k += 8) {
+        const int c = c0 + k, hw = hw0 + threadIdx.x;
+        if (c < C && hw < HW) {
+            if constexpr (sizeof(TX) == 2) tile[k][threadIdx.x] = __bfloat162float(xb[(int64_t)c * HW + hw]);
+            else tile[k][threadIdx.x] = xb[(int64_t)c * HW + hw];
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += 8) {
+        const int hw = hw0 + k, c = c0 + threadIdx.x;
+        if (c < C && hw < HW) yb[(int64_t)hw * C + c] = __float2bfloat16_rn(tile[threadIdx.x][k]);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool igemm_available() { return true; }
+
+static bool make_params(const IgemmShape &s, IgemmParams &prm) {
+    if (s.n % 2 != 0) return false;               // all four classes share one grid
+    if (s.c_in < 64 || s.c_in % 8 != 0) return false;
+    if (s.c_out % 16 != 0) return false;
+    if (s.x_dtype != SEGB_BF16 && s.x_dtype != SEGB_F32) return false;
+    if (s.y_dtype != SEGB_BF16 && s.y_dtype != SEGB_F32) return false;
+    if (s.batch > 65535) return false;
+    const int oh = 2 * s.h + 2 * s.pad - s.n, ow = 2 * s.w + 2 * s.pad - s.n;
+    if (oh < 2 || ow < 2) return false;
+    const int p = s.pad / 2, swap = s.pad & 1;
+    prm = IgemmParams{};
+    for (int c = 0; c < 4; ++c) {
+        const int r = c >> 1, q = c & 1;
+        ClassGeom &g = prm.cls[c];
+        g.R = sub_len(s.n, r);
+        g.C = sub_len(s.n, q);
+        g.st_r = (r + swap) % 2;
+        g.st_s = (q + swap) % 2;
+        g.rows = (oh - g.st_r + 1) / 2;
+        g.cols = (ow - g.st_s + 1) / 2;
+        g.base_r = (g.st_r + r) / 2;
+        g.base_s = (g.st_s + q) / 2;
+        g.tap0 = class_offset(s.n, c);
+    }
+    const int rows = prm.cls[0].rows, cols = prm.cls[0].cols;
+    for (int c = 1; c < 4; ++c)
+        if (prm.cls[c].rows != rows || prm.cls[c].cols != cols) return false;
+    // A box = 128 positions: (cols x rows x samples) rectangle of the class grid
+    if (cols >= kBlockM) {
+        if (cols % kBlockM) return false;
+        prm.box_w = kBlockM; prm.box_h = 1; prm.box_b = 1;
+    } else {
+        if (kBlockM % cols) return false;
+        prm.box_w = cols;
+        prm.box_h = std::min(rows, kBlockM / cols);
+        if (rows % prm.box_h) return false;
+        if (prm.box_h == rows) {
+            if (kBlockM % (cols * rows)) return false;
+            prm.box_b = kBlockM / (cols * rows);
+        } else {
+            if (prm.box_w * prm.box_h != kBlockM) return false;
+            prm.box_b = 1;
+        }
+    }
+    if (prm.box_b > 256 || prm.box_h > 256 || prm.box_w > 256) return false;
+    int nt = s.c_out <= 256 ? s.c_out : 0;
+    if (!nt)
+        for (int cand : {256, 128, 64, 32, 16})
+            if (s.c_out % cand == 0) { nt = cand; break; }
+    if (nt % 16 || nt > 256) return false;
+    if (nt % 32) return false;  // epilogue reads 32-column chunks
+    prm.n_tile = nt;
+    prm.n_blocks = s.c_out / nt;
+    prm.batch = (int)s.batch; prm.c_in = s.c_in; prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
+    prm.k_cblocks = (s.c_in + kBlockK - 1) / kBlockK;
+    prm.class_positions = s.batch * (int64_t)rows * cols;
+    prm.m_tiles = (int)ceil_div(prm.class_positions, kBlockM);
+    const int64_t total = 4ll * prm.m_tiles * prm.n_blocks;
+    if (total > INT32_MAX) return false;
+    prm.total_tiles = (int)total;
+    const int stage_bytes = kBlockM * kBlockK * 2 + nt * kBlockK * 2;
+    prm.stages = std::min(8, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
+    return prm.stages >= 2;
+}
+
+bool igemm_supported(const IgemmShape &s) {
+    IgemmParams prm;
+    return make_params(s, prm) && encode_fn() != nullptr;
+}
+
+int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
+    IgemmParams prm;
+    if (!make_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM: unsupported shape");
+    auto encode = encode_fn();
+    if (!encode) return fail(SEGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    // stage the channels-last bf16 A operand (stream-ordered workspace)
+    const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
+    void *xs = nullptr;
+    cudaError_t e = cudaMallocAsync(&xs, elems * 2, st);
+    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "workspace: %s", cudaGetErrorString(e));
+    {
+        dim3 blk(32, 8), grd((unsigned)ceil_div((int64_t)s.h * s.w, 32), (unsigned)ceil_div(s.c_in, 32),
+                             (unsigned)s.batch);
+        if (s.x_dtype == SEGB_BF16)
+            nchw_to_nhwc_bf16<__nv_bfloat16><<<grd, blk, 0, st>>>((const __nv_bfloat16 *)x, (__nv_bfloat16 *)xs,
+                                                                   s.c_in, s.h * s.w);
+        else
+            nchw_to_nhwc_bf16<float><<<grd, blk, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, s.h * s.w);
+        note_launch();
+        if (int rc = check_launch("nchw_to_nhwc_bf16")) { cudaFreeAsync(xs, st); return rc; }
+    }
+    CUtensorMap tmA, tmB;
+    {
+        cuuint64_t dims[4] = {(cuuint64_t)s.c_in, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.batch};
+        cuuint64_t strides[3] = {(cuuint64_t)s.c_in * 2, (cuuint64_t)s.w * s.c_in * 2,
+                                 (cuuint64_t)s.h * s.w * s.c_in * 2};
+        cuuint32_t box[4] = {(cuuint32_t)kBlockK, (cuuint32_t)prm.box_w, (cuuint32_t)prm.box_h, (cuuint32_t)prm.box_b};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        CUresult r = encode(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, xs, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { cudaFreeAsync(xs, st); return fail(SEGB_ERR_CUDA, "tensor map A: error %d", (int)r); }
+    }
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out, (cuuint64_t)s.n * s.n};
+        cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out * s.c_in_pad * 2};
+        cuuint32_t box[3] = {(cuuint32_t)kBlockK, (cuuint32_t)prm.n_tile, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box,
+                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { cudaFreeAsync(xs, st); return fail(SEGB_ERR_CUDA, "tensor map B: error %d", (int)r); }
+    }
+    prm.y = y;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t stage_bytes = (size_t)kBlockM * kBlockK * 2 + (size_t)prm.n_tile * kBlockK * 2;
+    const size_t smem = 1024 + prm.stages * stage_bytes + (2 * prm.stages + 4) * 8 + 16;
+    const unsigned grid = (unsigned)std::min<int64_t>(prm.total_tiles, sms);
+    if (s.y_dtype == SEGB_BF16) {
+        cudaFuncSetAttribute(igemm_tconv_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        igemm_tconv_kernel<__nv_bfloat16><<<grid, kThreads, smem, st>>>(tmA, tmB, prm);
+    } else {
+        cudaFuncSetAttribute(igemm_tconv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        igemm_tconv_kernel<float><<<grid, kThreads, smem, st>>>(tmA, tmB, prm);
+    }
+    note_launch();
+    int rc = check_launch("igemm_tconv_kernel");
+    cudaFreeAsync(xs, st);
+    return rc;
+}
+
 }  // namespace segb
