@@ -14,4 +14,8 @@ bool igemm_available();
 bool igemm_supported(const IgemmShape &s);
 int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st);
 
+// K3b: row-streaming variant for wide class grids (igemm_rows_sm100.cu)
+bool igemm_rows_supported(const IgemmShape &s);
+int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st);
+
 }  // namespace segb

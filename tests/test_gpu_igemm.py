@@ -107,3 +107,34 @@ def test_igemm_write_once_guard():
     torch.cuda.synchronize()
     assert not torch.isnan(y).any()
     assert torch.isnan(buf[:4096]).all() and torch.isnan(buf[4096 + total:]).all()
+
+
+ROWS_CASES = [  # K3b row-streaming variant: class grid cols % 128 == 0, c_out <= 64
+    ("ebgan_l7", 128, 128, 64, 4, 64, 2, 3),
+    ("rows_msub2", 32, 256, 64, 4, 32, 2, 2),
+    ("rows_kb2_n16", 16, 128, 128, 4, 16, 2, 2),
+    ("rows_odd_pad_n2", 16, 128, 64, 2, 32, 1, 2),
+    ("rows_n6_p3", 8, 128, 64, 6, 16, 3, 2),
+    ("rows_cin_tail", 16, 128, 40, 4, 48, 2, 2),
+]
+
+
+@pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", ROWS_CASES)
+def test_igemm_rows_variant(name, h, w, ci, n, co, pad, b, monkeypatch):
+    import torch
+    x, bank = _inputs(h, w, ci, n, co, b, 500 + w + ci)
+    xr = x.float().cpu().numpy().astype(np.float64)
+    br = O.bf16_round(bank).astype(np.float64)
+    ref = O.forward_segregated_batch(xr, br, pad)
+    layer = P.prepare_layer(bank, pad, compute="bf16")
+    y_rows = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
+    rep = O.compare(y_rows, ref, 1e-4, 1e-5)
+    assert rep["passed"], (name, rep)
+    yb = layer.forward(x, path="igemm").float().cpu().numpy()
+    assert O.compare(yb, ref, 2 ** -7, 1e-3 * float(np.abs(ref).max()))["passed"], name
+    monkeypatch.setenv("SEGB200_IGEMM_GENERIC", "1")  # the per-tap-box K3 variant, where eligible
+    try:
+        y_gen = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
+    except NotImplementedError:
+        return
+    assert O.compare(y_gen, ref, 1e-4, 1e-5)["passed"], name
