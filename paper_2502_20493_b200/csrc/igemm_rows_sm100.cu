@@ -1,31 +1,35 @@
 // K3b -- row-streaming implicit GEMM for wide class grids (cols % 128 == 0),
 // e.g. EB-GAN l7 (128x128x64 -> 256x256x64): all four parity classes of one
-// class-grid row (128 positions) per tile, weights resident, input rows loaded
-// once.
+// class-grid row (128 positions) per tile, weights resident, every input row
+// loaded once, output written by TMA.
 //
 // Same arithmetic as K3 (igemm_sm100.cu, per-class GEMMs of engines.py:271-335)
-// but the operand traffic is restructured for layers whose K = taps x c_in is
-// small and whose output is large, where K3's per-tap TMA boxes re-read every
-// input element n*n times from L2 and the weights once per tile:
+// with the operand traffic restructured for layers whose K = taps x c_in is
+// small and whose output is large (K3's per-tap boxes re-read each input
+// element n*n times and the weights once per tile):
 //   * weights: every (class, tap, 64-channel block) B tile is TMA-loaded once
 //     per CTA and stays resident in shared memory;
-//   * activations: NCHW rows are TMA-loaded raw (box {w, 1, 64 ch, 1}; the
-//     out-of-range columns/rows -- the floor(P/2) zero ring -- are TMA zero
-//     fill), then transposed by four warps into a ring of K-major SWIZZLE_128B
-//     "row slots" (slot row = input column, 64 channels = 128 B). No NHWC copy
-//     of the input ever touches HBM;
-//   * every (class, tap) A operand is a row-shifted view of a slot: the UMMA
-//     descriptor start address moves by 128 B per column shift (measured on
-//     B200: the SWIZZLE_128B phase follows the absolute smem address, so the
-//     descriptor's base-offset field stays 0);
-//   * consecutive class-grid rows of a strip share nr - 1 of their nr input rows,
-//     so each input row is loaded once per strip;
-//   * the epilogue holds all four classes of a position, so it writes the two
-//     output columns 2j, 2j+1 of both output rows as packed pairs (fully
-//     coalesced 128-B warp stores, every output element written once).
+//   * activations: four loader warps read NCHW input rows with 128-bit loads
+//     (the next row already in flight in registers), transpose 8x8 bf16 tiles
+//     with byte permutes and store them into a ring of K-major SWIZZLE_128B
+//     "row slots" (slot row = input column, 64 channels = 128 B); columns and
+//     rows outside the input -- the floor(P/2) zero ring -- are stored as
+//     zeros. No NHWC copy of the input touches HBM;
+//   * every A operand is a row-shifted view of a slot: the UMMA descriptor start
+//     moves by 128 B per column shift (measured on B200: the SWIZZLE_128B phase
+//     follows the absolute smem address, so the base-offset field stays 0);
+//   * (class, tap) pairs that read the same shifted window share one MMA: their
+//     B tiles are stored contiguously and their TMEM accumulators are adjacent,
+//     so e.g. the centre window of a 4x4 / P=2 layer feeds all four classes in a
+//     single N = 4*c_out MMA (11 MMAs per k-step instead of 16, 40% less smem
+//     operand traffic);
+//   * consecutive class-grid rows of a strip share nr - 1 of their nr input rows;
+//   * epilogue: TMEM -> registers -> bf16 pairs (output columns 2j, 2j+1 of both
+//     output rows) -> shared staging -> TMA tensor store of [co][2 rows][2*128]
+//     boxes; every output element written once.
 //
-// Warps: 0 TMA producer, 1 MMA issuer (+TMEM owner), 2..5 epilogue (TMEM lane
-// quarters), 6..9 transposers.
+// Warps: 0 weight TMA, 1 MMA issuer (+TMEM owner), 2..5 epilogue (TMEM lane
+// quarters), 6..9 row loaders / transposers.
 #include <cstdlib>
 #include <mutex>
 
@@ -35,47 +39,98 @@
 namespace segb {
 
 constexpr int kRowsThreads = 320;
-constexpr int kRing = 4;
-// raw row buffer: [64 ch][128] main box, then [64][8] left and right halo boxes
-constexpr uint32_t kRawMain = 64 * kBlockM * 2, kRawHalo = 64 * 8 * 2;
+constexpr int kRing = 4;            // input-row slots (power of two)
+constexpr int kStageBytes = 8192;   // one epilogue staging buffer (x2)
 
 struct RowsClass {
-    int R, C, st_r, st_s, base_r, base_s, tap0;
+    int st_r, st_s, base_r, base_s, tap0;
 };
 
 struct RowsParams {
     RowsClass cls[4];
-    int c_out, oh, ow, p;
-    int rows, msub;          // class-grid rows, 128-position subtiles per row
-    int dmin_r, nr;          // first window row offset, input rows per class-grid row
-    int dmin_c, slot_rows, raw_w;
-    int kbc, ntaps;          // 64-channel blocks, n*n
+    int c_in, c_out, h, w, oh, ow, p;
+    int rows, msub;  // class-grid rows, 128-position subtiles per row
+    int dmin_r, nr;  // first window row offset, input rows per class-grid row
+    int dmin_c, slot_rows;
     int total_tiles, tiles_per_cta;
-    uint32_t slot_bytes, raw_bytes, b_tile_bytes;
-    void *y;
+    uint32_t slot_bytes, b_tile_bytes;
+    const void *x;
 };
 
-struct RowsSmem {  // byte offsets from the 1024-aligned smem base
-    uint32_t b, ring, raw, bars, total;
+// ---------------------------------------------------------------------------
+// Compile-time MMA schedule for even n = 2*NH: A window (du, dc) of the slot
+// ring is shared by the classes (r, s) with 0 <= du - base_r < NH and
+// 0 <= dc - base_s < NH (base = parity when P is even, 0 when P is odd).
+struct MmaGroup {
+    int du, dc, c0, nc, b0;  // window, first class, class count, first B tile
 };
-
-__host__ __device__ inline RowsSmem rows_layout(const RowsParams &p) {
-    RowsSmem s;
-    s.b = 0;
-    s.ring = s.b + p.ntaps * p.kbc * p.b_tile_bytes;
-    s.raw = s.ring + kRing * p.kbc * p.slot_bytes;
-    s.bars = s.raw + ((p.raw_bytes + 1023) / 1024) * 1024;
-    s.total = s.bars + (3 + 2 * kRing * p.kbc + 4) * 8 + 16;
+template <int NH, int SWAP>
+struct Schedule {
+    MmaGroup g[(NH + 1) * (NH + 1) * 2];
+    int count = 0;
+    int btap[16 * 4];  // B tile k -> (class << 8) | (u << 4) | v
+    bool fresh[(NH + 1) * (NH + 1) * 2];
+};
+template <int NH, int SWAP>
+constexpr Schedule<NH, SWAP> make_schedule() {
+    Schedule<NH, SWAP> s{};
+    const int W = SWAP ? NH : NH + 1;  // distinct windows per axis
+    int nb = 0;
+    auto add = [&](int du, int dc, int c0, int nc) {
+        s.g[s.count] = MmaGroup{du, dc, c0, nc, nb};
+        for (int c = c0; c < c0 + nc; ++c) {
+            const int r = c >> 1, q = c & 1;
+            const int u = du - (SWAP ? 0 : r), v = dc - (SWAP ? 0 : q);
+            s.btap[nb++] = (c << 8) | (u << 4) | v;
+        }
+        s.count++;
+    };
+    // windows feeding all four classes first, so one MMA initialises every accumulator
+    for (int pass = 0; pass < 2; ++pass)
+        for (int du = 0; du < W; ++du)
+            for (int dc = 0; dc < W; ++dc) {
+                bool rr[2] = {false, false}, ss[2] = {false, false};
+                for (int r = 0; r < 2; ++r) {
+                    const int u = du - (SWAP ? 0 : r), v = dc - (SWAP ? 0 : r);
+                    rr[r] = u >= 0 && u < NH;
+                    ss[r] = v >= 0 && v < NH;
+                }
+                const bool full = rr[0] && rr[1] && ss[0] && ss[1];
+                if ((pass == 0) != full) continue;
+                if (full) {
+                    add(du, dc, 0, 4);
+                    continue;
+                }
+                for (int r = 0; r < 2; ++r) {
+                    if (!rr[r]) continue;
+                    if (ss[0] && ss[1]) {
+                        add(du, dc, 2 * r, 2);
+                    } else {
+                        for (int q = 0; q < 2; ++q)
+                            if (ss[q]) add(du, dc, 2 * r + q, 1);
+                    }
+                }
+            }
+    bool touched[4] = {false, false, false, false};
+    for (int i = 0; i < s.count; ++i) {
+        s.fresh[i] = !touched[s.g[i].c0];
+        for (int c = s.g[i].c0; c < s.g[i].c0 + s.g[i].nc; ++c) touched[c] = true;
+    }
     return s;
 }
 
-template <typename TY> __device__ __forceinline__ void store_pair(TY *dst, float lo, float hi);
-template <> __device__ __forceinline__ void store_pair<__nv_bfloat16>(__nv_bfloat16 *dst, float lo, float hi) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    *reinterpret_cast<__nv_bfloat162 *>(dst) = v;
-}
-template <> __device__ __forceinline__ void store_pair<float>(float *dst, float lo, float hi) {
-    *reinterpret_cast<float2 *>(dst) = make_float2(lo, hi);
+struct RowsSmem {  // byte offsets from the 1024-aligned smem base
+    uint32_t b, ring, stage, bars, total;
+};
+
+__host__ __device__ inline RowsSmem rows_layout(const RowsParams &p, int ntaps, int kbc) {
+    RowsSmem s;
+    s.b = 0;
+    s.ring = s.b + ntaps * kbc * p.b_tile_bytes;
+    s.stage = s.ring + kRing * kbc * p.slot_bytes;
+    s.bars = s.stage + 2 * kStageBytes;
+    s.total = s.bars + (1 + 2 * kRing * kbc + 4) * 8 + 16;
+    return s;
 }
 
 // number of input-row loads a tile triggers (nr when it starts a strip, else 1)
@@ -83,36 +138,51 @@ __device__ __forceinline__ int tile_loads(const RowsParams &p, int t, int t0) {
     return (t == t0 || (t % p.rows) == 0) ? p.nr : 1;
 }
 
-template <typename TY>
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, uint32_t src, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&v);
+}
+
+template <int NH, int KBC, int SWAP>
 __global__ void __launch_bounds__(kRowsThreads, 1)
-    igemm_rows_kernel(const __grid_constant__ CUtensorMap tmRaw, const __grid_constant__ CUtensorMap tmHalo,
-                      const __grid_constant__ CUtensorMap tmB,
+    igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
                       const RowsParams prm) {
+    constexpr int NTAPS = 4 * NH * NH;
+    constexpr Schedule<NH, SWAP> SCH = make_schedule<NH, SWAP>();
+    constexpr int CC = kStageBytes / (2 * 2 * kBlockM * 2);  // bf16 output channels per staged box (8)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const RowsSmem L = rows_layout(prm);
+    const RowsSmem L = rows_layout(prm, NTAPS, KBC);
     uint8_t *sB = smem + L.b;
     uint8_t *sRing = smem + L.ring;
-    uint8_t *sRaw = smem + L.raw;
+    uint8_t *sStage = smem + L.stage;
     uint64_t *b_full = reinterpret_cast<uint64_t *>(smem + L.bars);
-    uint64_t *raw_full = b_full + 1;
-    uint64_t *raw_empty = b_full + 2;
-    uint64_t *slot_full = b_full + 3;
-    uint64_t *slot_empty = slot_full + kRing * prm.kbc;
-    uint64_t *tfull = slot_empty + kRing * prm.kbc;
+    uint64_t *slot_full = b_full + 1;
+    uint64_t *slot_empty = slot_full + kRing * KBC;
+    uint64_t *tfull = slot_empty + kRing * KBC;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int N = prm.c_out;
-    const int nslots = kRing * prm.kbc;
 
     if (threadIdx.x == 0) {
         mbar_init(b_full, 1);
-        mbar_init(raw_full, 1);
-        mbar_init(raw_empty, 4);
-        for (int i = 0; i < nslots; ++i) {
-            mbar_init(&slot_full[i], 4);
+        for (int i = 0; i < kRing * KBC; ++i) {
+            mbar_init(&slot_full[i], 4);  // one arrival per loader warp
             mbar_init(&slot_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -120,9 +190,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             mbar_init(&tempty[i], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmRaw) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmHalo) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmY) : "memory");
     }
     const uint32_t tcols = tmem_pow2(8 * N);  // 2 buffers x 4 classes x N fp32 columns
     if (warp == 1) {
@@ -134,174 +203,208 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-
     const int t0 = blockIdx.x * prm.tiles_per_cta;
     const int t1 = min(prm.total_tiles, t0 + prm.tiles_per_cta);
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- producer: resident weights, then raw input rows
-            mbar_expect_tx(b_full, prm.ntaps * prm.kbc * prm.b_tile_bytes);
-            for (int tap = 0; tap < prm.ntaps; ++tap)
-                for (int kb = 0; kb < prm.kbc; ++kb)
-                    tma_load_3d(sB + (tap * prm.kbc + kb) * prm.b_tile_bytes, &tmB, b_full, kb * 64, 0, tap);
-            uint32_t g = 0;
-            for (int t = t0; t < t1; ++t) {
-                const int i = t % prm.rows, rest = t / prm.rows;
-                const int ms = rest % prm.msub, b = rest / prm.msub;
-                const int nl = tile_loads(prm, t, t0);
-                for (int l = prm.nr - nl; l < prm.nr; ++l) {
-                    const int row = i + prm.dmin_r + l;
-                    for (int kb = 0; kb < prm.kbc; ++kb, ++g) {
-                        mbar_wait(raw_empty, (g & 1) ^ 1);
-                        // main 128 columns + 8-column halo boxes left and right (a box
-                        // may not be wider than the tensor, so the halo is separate)
-                        const int j0 = ms * kBlockM;
-                        mbar_expect_tx(raw_full, prm.raw_bytes);
-                        tma_load_4d(sRaw, &tmRaw, raw_full, j0, row, kb * 64, b);
-                        tma_load_4d(sRaw + kRawMain, &tmHalo, raw_full, j0 - 8, row, kb * 64, b);
-                        tma_load_4d(sRaw + kRawMain + kRawHalo, &tmHalo, raw_full, j0 + kBlockM, row, kb * 64, b);
-                    }
-                }
+        if (lane == 0) {  // ---------------- the resident weights, in schedule order
+            mbar_expect_tx(b_full, NTAPS * KBC * prm.b_tile_bytes);
+#pragma unroll
+            for (int k = 0; k < NTAPS; ++k) {
+                const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
+                const int tap = prm.cls[c].tap0 + u * NH + v;
+                for (int kb = 0; kb < KBC; ++kb)  // [kb][k]: a group's B tiles stay contiguous
+                    tma_load_3d(sB + (kb * NTAPS + k) * prm.b_tile_bytes, &tmB, b_full, kb * 64, 0, tap);
             }
         }
-    } else if (warp >= 6) {  // ---------------- transposers: raw [64 ch][raw_w] -> K-major SW128 slot rows
-        const int tw = warp - 6;
-        const uint16_t *raw = reinterpret_cast<const uint16_t *>(sRaw);
-        const int nblk = (prm.slot_rows + 31) / 32;
-        uint32_t g = 0, q = 0;
-        for (int t = t0; t < t1; ++t) {
-            const int nl = tile_loads(prm, t, t0);
-            for (int l = 0; l < nl; ++l, ++q) {
-                const int k = q % kRing;
-                const uint32_t use = q / kRing;
-                for (int kb = 0; kb < prm.kbc; ++kb, ++g) {
-                    const int sidx = k * prm.kbc + kb;
-                    mbar_wait(&slot_empty[sidx], (use & 1) ^ 1);
-                    mbar_wait(raw_full, g & 1);
-                    const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
-                    for (int task = tw; task < 8 * nblk; task += 4) {
-                        const int k8 = task & 7, rho = (task >> 3) * 32 + lane;
-                        if (rho < prm.slot_rows) {
-                            uint32_t w[4];
+    } else if (warp >= 6) {
+        // ---------------- row loaders / transposers: NCHW input row (64 channels x 128 columns
+        // + halo) -> K-major SWIZZLE_128B slot rows. Thread (cg = t & 7, cc = t >> 3) loads 8
+        // channels x 8 columns with 128-bit loads (coalesced along the row), transposes the 8x8
+        // bf16 tile in registers and stores 8 slot rows x 16 B; the next unit's loads are in
+        // flight while the current one is stored.
+        const int tt = threadIdx.x - 6 * 32;
+        const int cg = tt & 7, cc = tt >> 3;
+        const int HL = -prm.dmin_c, HR = prm.slot_rows - kBlockM - HL;
+        const __nv_bfloat16 *x = reinterpret_cast<const __nv_bfloat16 *>(prm.x);
+        const int64_t plane_in = (int64_t)prm.h * prm.w;
+        auto load_unit = [&](int t, int l, int kb, uint4 (&r)[8], uint4 &hv) {
+            const int i = t % prm.rows, rest = t / prm.rows;
+            const int ms = rest % prm.msub, b = rest / prm.msub;
+            const int row = i + prm.dmin_r + l;
+            const int j0 = ms * kBlockM;
+            const bool rok = row >= 0 && row < prm.h;
+            const int ch0 = kb * 64 + cg * 8;
+            const __nv_bfloat16 *src = x + ((int64_t)b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
 #pragma unroll
-                            // slot row rho <-> input column j0 + dmin_c + rho
-                            const int o = rho + prm.dmin_c;
-                            const uint16_t *src;
-                            int pitch;
-                            if (o < 0) { src = raw + kRawMain / 2 + 8 + o; pitch = 8; }
-                            else if (o >= kBlockM) { src = raw + (kRawMain + kRawHalo) / 2 + (o - kBlockM); pitch = 8; }
-                            else { src = raw + o; pitch = kBlockM; }
-                            for (int e = 0; e < 4; ++e) {
-                                const uint32_t lo = src[(8 * k8 + 2 * e) * pitch];
-                                const uint32_t hi = src[(8 * k8 + 2 * e + 1) * pitch];
-                                w[e] = lo | (hi << 16);
-                            }
-                            const uint32_t addr = dst + rho * 128 + ((k8 ^ (rho & 7)) << 4);
-                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]),
-                                         "r"(w[1]), "r"(w[2]), "r"(w[3])
-                                         : "memory");
-                        }
-                    }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&slot_full[sidx]);
-                        mbar_arrive(raw_empty);
-                    }
+            for (int c = 0; c < 8; ++c) {
+                r[c] = make_uint4(0, 0, 0, 0);
+                if (rok && ch0 + c < prm.c_in)
+                    r[c] = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)c * plane_in + cc * 8));
+            }
+            hv = make_uint4(0, 0, 0, 0);
+            if (tt < (HL + HR) * 8) {  // halo column tasks: (halo col, channel group)
+                const int hc = tt >> 3;
+                const int col = hc < HL ? j0 - HL + hc : j0 + kBlockM + (hc - HL);
+                if (rok && col >= 0 && col < prm.w) {
+                    uint32_t h16[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        h16[c] = (ch0 + c < prm.c_in)
+                                     ? (uint32_t)__ldg(reinterpret_cast<const unsigned short *>(
+                                           src + (int64_t)c * plane_in + (col - j0)))
+                                     : 0u;
+                    hv = make_uint4(h16[0] | (h16[1] << 16), h16[2] | (h16[3] << 16), h16[4] | (h16[5] << 16),
+                                    h16[6] | (h16[7] << 16));
                 }
             }
+        };
+        int pt = t0, pl = t0 < t1 ? prm.nr - tile_loads(prm, t0, t0) : 0, pkb = 0;
+        uint4 cur[8], hcur;
+        if (pt < t1) load_unit(pt, pl, pkb, cur, hcur);
+        uint32_t q = 0;
+        while (pt < t1) {
+            const int ckb = pkb;
+            if (++pkb == KBC) {
+                pkb = 0;
+                if (++pl == prm.nr && ++pt < t1) pl = prm.nr - tile_loads(prm, pt, t0);
+            }
+            uint4 nxt[8], hnxt;
+            if (pt < t1) load_unit(pt, pl, pkb, nxt, hnxt);
+            const int sidx = (q & (kRing - 1)) * KBC + ckb;
+            mbar_wait(&slot_empty[sidx], ((q / kRing) & 1) ^ 1);
+            const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
+                uint32_t o[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const uint32_t a = (&cur[2 * m].x)[w >> 1], bb = (&cur[2 * m + 1].x)[w >> 1];
+                    o[m] = __byte_perm(a, bb, (w & 1) ? 0x7632 : 0x5410);
+                }
+                const int rho = HL + cc * 8 + w;
+                const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+                             "r"(o[3])
+                             : "memory");
+            }
+            if (tt < (HL + HR) * 8) {
+                const int hc = tt >> 3;
+                const int rho = hc < HL ? hc : HL + kBlockM + (hc - HL);
+                const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(hcur.x), "r"(hcur.y),
+                             "r"(hcur.z), "r"(hcur.w)
+                             : "memory");
+            }
+            fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&slot_full[sidx]);
+            if (ckb == KBC - 1) ++q;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) cur[c] = nxt[c];
+            hcur = hnxt;
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            mbar_wait(b_full, 0);
-            const uint32_t idesc = idesc_bf16(N);
-            const uint32_t ring0 = smem_u32(sRing), b0 = smem_u32(sB);
-            int acc = 0;
-            uint32_t acc_phase = 0, qe = 0;
-            for (int t = t0; t < t1; ++t) {
-                qe += tile_loads(prm, t, t0);
-                const uint32_t qbase = qe - prm.nr;
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                for (int l = 0; l < prm.nr; ++l) {
-                    const uint32_t q = qbase + l;
-                    for (int kb = 0; kb < prm.kbc; ++kb)
-                        mbar_wait(&slot_full[(q % kRing) * prm.kbc + kb], (q / kRing) & 1);
-                }
-                tc_fence_after();
-                for (int c = 0; c < 4; ++c) {
-                    const RowsClass &g = prm.cls[c];
-                    const uint32_t d = tmem_base + acc * 4 * N + c * N;
-                    uint32_t accumulate = 0;
-                    for (int u = 0; u < g.R; ++u) {
-                        const uint32_t q = qbase + (g.base_r + u - prm.p - prm.dmin_r);
-                        for (int v = 0; v < g.C; ++v) {
-                            const uint32_t dc = g.base_s + v - prm.p - prm.dmin_c;
-                            const int tap = g.tap0 + u * g.C + v;
-                            for (int kb = 0; kb < prm.kbc; ++kb) {
-                                const uint32_t a_addr = ring0 + ((q % kRing) * prm.kbc + kb) * prm.slot_bytes + dc * 128;
-                                const uint32_t b_addr = b0 + (tap * prm.kbc + kb) * prm.b_tile_bytes;
+        // ---------------- MMA issuer: the whole warp walks the compile-time schedule (uniform
+        // values), one elected lane issues each tcgen05.mma.
+        mbar_wait(b_full, 0);
+        const uint64_t dA0 = desc_k_sw128(smem_u32(sRing)), dB0 = desc_k_sw128(smem_u32(sB));
+        const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
+        int acc = 0;
+        uint32_t acc_phase = 0, qe = 0;
+        for (int t = t0; t < t1; ++t) {
+            qe += tile_loads(prm, t, t0);
+            const uint32_t qbase = qe - prm.nr;
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            for (int l = 0; l < prm.nr; ++l) {
+                const uint32_t q = qbase + l;
 #pragma unroll
-                                for (int kk = 0; kk < 4; ++kk) {
-                                    // row-shifted start address; the SW128 pattern follows the
-                                    // absolute smem address bits, so no base offset is needed
-                                    tc_mma(d, desc_k_sw128(a_addr + kk * 32), desc_k_sw128(b_addr + kk * 32),
-                                           idesc, accumulate);
-                                    accumulate = 1;
-                                }
-                            }
-                        }
-                    }
-                }
+                for (int kb = 0; kb < KBC; ++kb) mbar_wait(&slot_full[(q & (kRing - 1)) * KBC + kb], (q / kRing) & 1);
+            }
+            tc_fence_after();
+            const uint32_t d0 = tmem_base + acc * 4 * N;
+#pragma unroll
+            for (int gi = 0; gi < SCH.count; ++gi) {
+                const MmaGroup g = SCH.g[gi];
+                const uint32_t arow = ((qbase + g.du) & (kRing - 1)) * KBC * S16 + g.dc * 8;
+                const uint32_t idesc = idesc_bf16(g.nc * N);
+#pragma unroll
+                for (int kb = 0; kb < KBC; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        if (elect_one())
+                            tc_mma(d0 + g.c0 * N, dA0 + arow + kb * S16 + kk * 2, dB0 + (kb * NTAPS + g.b0) * B16 + kk * 2,
+                                   idesc, (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u);
+            }
+            if (elect_one()) {
                 tc_commit(&tfull[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 // release input rows no later tile of this strip reads
                 const bool cont = (t + 1 < t1) && ((t + 1) % prm.rows != 0);
                 const int nrel = cont ? 1 : prm.nr;
                 for (int l = 0; l < nrel; ++l) {
                     const uint32_t q = qbase + l;
-                    for (int kb = 0; kb < prm.kbc; ++kb) tc_commit(&slot_empty[(q % kRing) * prm.kbc + kb]);
+#pragma unroll
+                    for (int kb = 0; kb < KBC; ++kb) tc_commit(&slot_empty[(q & (kRing - 1)) * KBC + kb]);
                 }
             }
+            __syncwarp();
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-    } else {  // ---------------- epilogue (warps 2..5): TMEM lane quarter = warp % 4
+    } else {
+        // ---------------- epilogue (warps 2..5; TMEM lane quarter = warp % 4). Per chunk of CC
+        // output channels: TMEM -> packed bf16 pairs -> staging [co][2 rows][256] -> TMA store.
         const int quarter = warp & 3;
-        const int m = quarter * 32 + lane;
-        const int64_t plane = (int64_t)prm.oh * prm.ow;
-        TY *y = reinterpret_cast<TY *>(prm.y);
-        // y = 2j + st_s: the class with st_s == 0 fills the even column of the pair
-        const int s_even = prm.cls[0].st_s == 0 ? 0 : 1;
+        const int m = quarter * 32 + lane;  // position within the 128-wide subtile
+        const bool leader = (warp == 2 && lane == 0);
+        const int s_even = prm.cls[0].st_s == 0 ? 0 : 1;  // class column parity filling even columns
+        const int rlo = prm.cls[0].st_r == 0 ? 0 : 1;     // class row parity of staging row 0 (row 2i)
         int acc = 0;
-        uint32_t acc_phase = 0;
+        uint32_t acc_phase = 0, chunk = 0;
         for (int t = t0; t < t1; ++t) {
             const int i = t % prm.rows, rest = t / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
-            const int j = ms * kBlockM + m;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            TY *base = y + (int64_t)b * N * plane + 2 * j;
-            for (int ch = 0; ch < N; ch += 16) {
-                uint32_t v[4][16];
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 4 * N;
+            for (int co0 = 0; co0 < N; co0 += CC, ++chunk) {
+                uint32_t v[4][CC];
 #pragma unroll
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 4 * N + c * N + ch, v[c]);
+                for (int c = 0; c < 4; ++c) tmem_ld8(tl + c * N + co0, v[c]);
                 tmem_wait_ld();
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int x = 2 * i + prm.cls[2 * r].st_r;
+                for (int c = 0; c < 4; ++c) reg_fence8(v[c]);
+                if (co0 + CC >= N) {  // last chunk of the tile: release the accumulator buffer
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                }
+                // staging buffer `chunk & 1` is free once the store issued two chunks ago has read it
+                if (leader) bulk_wait_read1();
+                named_bar(1, 128);
+                const uint32_t stg = smem_u32(sStage + (chunk & 1) * kStageBytes);
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const float a0 = __uint_as_float(v[2 * r][k]), a1 = __uint_as_float(v[2 * r + 1][k]);
-                        store_pair<TY>(base + (int64_t)(ch + k) * plane + (int64_t)x * prm.ow, s_even ? a1 : a0,
-                                       s_even ? a0 : a1);
+                for (int k = 0; k < CC; ++k) {
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const bool r1 = (rr ^ rlo) != 0;  // class row parity stored at staging row rr
+                        const float a0 = __uint_as_float(r1 ? v[2][k] : v[0][k]);
+                        const float a1 = __uint_as_float(r1 ? v[3][k] : v[1][k]);
+                        const uint32_t addr = stg + ((k * 2 + rr) * 2 * kBlockM + 2 * m) * 2;
+                        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr),
+                                     "r"(pack_bf16x2(s_even ? a1 : a0, s_even ? a0 : a1))
+                                     : "memory");
                     }
                 }
+                fence_proxy_async_smem();
+                named_bar(1, 128);
+                if (leader) {
+                    tma_store_4d(&tmY, stg, ms * 2 * kBlockM, 2 * i, co0, b);
+                    bulk_commit();
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (leader) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -312,74 +415,70 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
-
-static bool rows_params(const IgemmShape &s, RowsParams &prm) {
-    if (s.n % 2 != 0 || s.x_dtype != SEGB_BF16) return false;
-    if (s.y_dtype != SEGB_BF16 && s.y_dtype != SEGB_F32) return false;
+static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc, int &swap) {
+    if (s.n % 2 != 0 || s.n > 6 || s.x_dtype != SEGB_BF16) return false;
+    if (s.y_dtype != SEGB_BF16) return false;  // fp32 output takes K3 (the staging is sized for bf16)
     if (s.c_out < 16 || s.c_out > 64 || s.c_out % 16 != 0) return false;
-    if (s.w % 8 != 0) return false;  // TMA: NCHW row pitch must be a multiple of 16 B
+    if (s.w % 8 != 0 || s.w < kBlockM) return false;
     const int oh = 2 * s.h + 2 * s.pad - s.n, ow = 2 * s.w + 2 * s.pad - s.n;
     if (oh < 2 || ow < 2) return false;
-    const int p = s.pad / 2, swap = s.pad & 1;
+    const int p = s.pad / 2;
+    swap = s.pad & 1;
+    nh = s.n / 2;
     prm = RowsParams{};
     int dmin_r = 1 << 30, dmax_r = -(1 << 30), dmin_c = 1 << 30, dmax_c = -(1 << 30);
     for (int c = 0; c < 4; ++c) {
         const int r = c >> 1, q = c & 1;
         RowsClass &g = prm.cls[c];
-        g.R = sub_len(s.n, r);
-        g.C = sub_len(s.n, q);
         g.st_r = (r + swap) % 2;
         g.st_s = (q + swap) % 2;
         g.base_r = (g.st_r + r) / 2;
         g.base_s = (g.st_s + q) / 2;
         g.tap0 = class_offset(s.n, c);
         dmin_r = std::min(dmin_r, g.base_r - p);
-        dmax_r = std::max(dmax_r, g.base_r + g.R - 1 - p);
+        dmax_r = std::max(dmax_r, g.base_r + nh - 1 - p);
         dmin_c = std::min(dmin_c, g.base_s - p);
-        dmax_c = std::max(dmax_c, g.base_s + g.C - 1 - p);
+        dmax_c = std::max(dmax_c, g.base_s + nh - 1 - p);
     }
     const int rows = oh / 2, cols = ow / 2;
     if (cols % kBlockM != 0) return false;
+    prm.c_in = s.c_in; prm.h = s.h; prm.w = s.w;
     prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
     prm.rows = rows; prm.msub = cols / kBlockM;
     prm.dmin_r = dmin_r; prm.nr = dmax_r - dmin_r + 1;
     prm.dmin_c = dmin_c;
     prm.slot_rows = kBlockM + dmax_c - dmin_c;
-    prm.raw_w = kBlockM;
     if (-dmin_c > 8 || dmax_c > 8 || prm.nr > kRing) return false;
-    if (s.w < kBlockM) return false;
-    prm.kbc = (s.c_in + 63) / 64;
-    prm.ntaps = s.n * s.n;
+    kbc = (s.c_in + 63) / 64;
+    if (kbc > 2) return false;
     prm.slot_bytes = (prm.slot_rows * 128 + 1023) / 1024 * 1024;
-    prm.raw_bytes = kRawMain + 2 * kRawHalo;
     prm.b_tile_bytes = s.c_out * 128;
     const int64_t total = s.batch * (int64_t)prm.msub * rows;
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
-    return rows_layout(prm).total + 1024 <= 227 * 1024;
+    return rows_layout(prm, s.n * s.n, kbc).total + 1024 <= 227 * 1024;
 }
 
 bool igemm_rows_supported(const IgemmShape &s) {
     RowsParams prm;
-    return rows_params(s, prm) && tensor_map_encoder() != nullptr;
+    int nh, kbc, swap;
+    return rows_params(s, prm, nh, kbc, swap) && tensor_map_encoder() != nullptr;
+}
+
+template <int NH, int KBC, int SWAP>
+static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const CUtensorMap &tmY,
+                        const RowsParams &prm) {
+    cudaFuncSetAttribute(igemm_rows_kernel<NH, KBC, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    igemm_rows_kernel<NH, KBC, SWAP><<<grid, kRowsThreads, smem, st>>>(tmB, tmY, prm);
 }
 
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
     RowsParams prm;
-    if (!rows_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: unsupported shape");
+    int nh, kbc, swap;
+    if (!rows_params(s, prm, nh, kbc, swap))
+        return fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: unsupported shape");
     auto encode = tensor_map_encoder();
-    CUtensorMap tmRaw, tmHalo, tmB;
-    for (int k = 0; k < 2; ++k) {
-        cuuint64_t dims[4] = {(cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.c_in, (cuuint64_t)s.batch};
-        cuuint64_t strides[3] = {(cuuint64_t)s.w * 2, (cuuint64_t)s.h * s.w * 2, (cuuint64_t)s.c_in * s.h * s.w * 2};
-        cuuint32_t box[4] = {k == 0 ? (cuuint32_t)kBlockM : 8u, 1, 64, 1};
-        cuuint32_t es[4] = {1, 1, 1, 1};
-        CUresult r = encode(k == 0 ? &tmRaw : &tmHalo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims,
-                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (raw rows): error %d", (int)r);
-    }
+    CUtensorMap tmB, tmY;
     {
         cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out, (cuuint64_t)s.n * s.n};
         cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out * s.c_in_pad * 2};
@@ -390,20 +489,34 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (weights): error %d", (int)r);
     }
-    prm.y = y;
+    {
+        const int cc = kStageBytes / (2 * 2 * kBlockM * 2);
+        cuuint64_t dims[4] = {(cuuint64_t)prm.ow, (cuuint64_t)prm.oh, (cuuint64_t)s.c_out, (cuuint64_t)s.batch};
+        cuuint64_t strides[3] = {(cuuint64_t)prm.ow * 2, (cuuint64_t)prm.oh * prm.ow * 2,
+                                 (cuuint64_t)s.c_out * prm.oh * prm.ow * 2};
+        cuuint32_t box[4] = {2 * kBlockM, 2, (cuuint32_t)cc, 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        CUresult r = encode(&tmY, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (output): error %d", (int)r);
+    }
+    prm.x = x;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)std::min<int64_t>(prm.total_tiles, sms);
     prm.tiles_per_cta = (int)ceil_div(prm.total_tiles, grid);
-    const size_t smem = rows_layout(prm).total + 1024;
-    if (s.y_dtype == SEGB_BF16) {
-        cudaFuncSetAttribute(igemm_rows_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        igemm_rows_kernel<__nv_bfloat16><<<grid, kRowsThreads, smem, st>>>(tmRaw, tmHalo, tmB, prm);
-    } else {
-        cudaFuncSetAttribute(igemm_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        igemm_rows_kernel<float><<<grid, kRowsThreads, smem, st>>>(tmRaw, tmHalo, tmB, prm);
-    }
+    const size_t smem = rows_layout(prm, s.n * s.n, kbc).total + 1024;
+    int rc = SEGB_OK;
+#define SEGB_ROWS_CASE(NH_, KBC_, SW_) \
+    if (nh == NH_ && kbc == KBC_ && swap == SW_) launch_rows<NH_, KBC_, SW_>(grid, smem, st, tmB, tmY, prm); else
+    SEGB_ROWS_CASE(1, 1, 0) SEGB_ROWS_CASE(1, 1, 1) SEGB_ROWS_CASE(1, 2, 0) SEGB_ROWS_CASE(1, 2, 1)
+    SEGB_ROWS_CASE(2, 1, 0) SEGB_ROWS_CASE(2, 1, 1) SEGB_ROWS_CASE(2, 2, 0) SEGB_ROWS_CASE(2, 2, 1)
+    SEGB_ROWS_CASE(3, 1, 0) SEGB_ROWS_CASE(3, 1, 1) SEGB_ROWS_CASE(3, 2, 0) SEGB_ROWS_CASE(3, 2, 1)
+    { rc = fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: variant not instantiated"); }
+#undef SEGB_ROWS_CASE
+    if (rc) return rc;
     note_launch();
     return check_launch("igemm_rows_kernel");
 }
