@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // NCHW (bf16 or fp32) -> NHWC bf16 staging: the channels-last A operand.
+// Generic fallback (any HW): 32x32 shared-memory tile transpose.
 template <typename TX>
 __global__ void nchw_to_nhwc_bf16(const TX *__restrict__ x, __nv_bfloat16 *__restrict__ y, int C, int HW) {
     __shared__ float tile[32][33];
@@ -218,6 +219,46 @@ __global__ void nchw_to_nhwc_bf16(const TX *__restrict__ x, __nv_bfloat16 *__res
     for (int k = threadIdx.y; k < 32; k += 8) {
         const int hw = hw0 + k, c = c0 + threadIdx.x;
         if (c < C && hw < HW) yb[(int64_t)hw * C + c] = __float2bfloat16_rn(tile[threadIdx.x][k]);
+    }
+}
+
+// Vectorised path (HW % 8 == 0, C % 8 == 0): thread (cg = t & 7, hc = t >> 3) of a
+// 256-thread block loads an 8-channel x 8-position tile with 128-bit loads, transposes
+// it in registers with byte permutes and writes 8 x 128-bit channels-last rows.
+// Block tile: 64 channels x 256 positions; no shared memory.
+template <typename TX>
+__global__ void __launch_bounds__(256) nchw_to_nhwc_bf16_v8(const TX *__restrict__ x, __nv_bfloat16 *__restrict__ y,
+                                                             int C, int HW) {
+    const int64_t b = blockIdx.z;
+    const int cg = threadIdx.x & 7, hc = threadIdx.x >> 3;
+    const int c0 = blockIdx.y * 64 + cg * 8;
+    const int hw0 = blockIdx.x * 256 + hc * 8;
+    if (c0 >= C || hw0 >= HW) return;
+    const TX *src = x + (b * C + c0) * (int64_t)HW + hw0;
+    uint32_t r[8][4];  // r[c][k]: channel c, positions 2k, 2k+1 (bf16 pairs)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        if constexpr (sizeof(TX) == 2) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)c * HW));
+            r[c][0] = v.x; r[c][1] = v.y; r[c][2] = v.z; r[c][3] = v.w;
+        } else {
+            const float4 a = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)c * HW));
+            const float4 bb = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)c * HW + 4));
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w);
+            __nv_bfloat162 p2 = __floats2bfloat162_rn(bb.x, bb.y), p3 = __floats2bfloat162_rn(bb.z, bb.w);
+            r[c][0] = *reinterpret_cast<uint32_t *>(&p0); r[c][1] = *reinterpret_cast<uint32_t *>(&p1);
+            r[c][2] = *reinterpret_cast<uint32_t *>(&p2); r[c][3] = *reinterpret_cast<uint32_t *>(&p3);
+        }
+    }
+    __nv_bfloat16 *dst = y + (b * HW + hw0) * (int64_t)C + c0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        uint4 o;
+        uint32_t *op = &o.x;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            op[m] = __byte_perm(r[2 * m][w >> 1], r[2 * m + 1][w >> 1], (w & 1) ? 0x7632 : 0x5410);
+        *reinterpret_cast<uint4 *>(dst + (int64_t)w * C) = o;
     }
 }
 
@@ -335,13 +376,22 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaS
     cudaError_t e = cudaMallocAsync(&xs, elems * 2, st);
     if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "workspace: %s", cudaGetErrorString(e));
     {
-        dim3 blk(32, 8), grd((unsigned)ceil_div((int64_t)s.h * s.w, 32), (unsigned)ceil_div(s.c_in, 32),
-                             (unsigned)s.batch);
-        if (s.x_dtype == SEGB_BF16)
-            nchw_to_nhwc_bf16<__nv_bfloat16><<<grd, blk, 0, st>>>((const __nv_bfloat16 *)x, (__nv_bfloat16 *)xs,
-                                                                   s.c_in, s.h * s.w);
-        else
-            nchw_to_nhwc_bf16<float><<<grd, blk, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, s.h * s.w);
+        const int hw = s.h * s.w;
+        if (hw % 8 == 0 && s.c_in % 8 == 0) {
+            dim3 grd((unsigned)ceil_div(hw, 256), (unsigned)ceil_div(s.c_in, 64), (unsigned)s.batch);
+            if (s.x_dtype == SEGB_BF16)
+                nchw_to_nhwc_bf16_v8<__nv_bfloat16><<<grd, 256, 0, st>>>((const __nv_bfloat16 *)x,
+                                                                         (__nv_bfloat16 *)xs, s.c_in, hw);
+            else
+                nchw_to_nhwc_bf16_v8<float><<<grd, 256, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw);
+        } else {
+            dim3 blk(32, 8), grd((unsigned)ceil_div(hw, 32), (unsigned)ceil_div(s.c_in, 32), (unsigned)s.batch);
+            if (s.x_dtype == SEGB_BF16)
+                nchw_to_nhwc_bf16<__nv_bfloat16><<<grd, blk, 0, st>>>((const __nv_bfloat16 *)x, (__nv_bfloat16 *)xs,
+                                                                       s.c_in, hw);
+            else
+                nchw_to_nhwc_bf16<float><<<grd, blk, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw);
+        }
         note_launch();
         if (int rc = check_launch("nchw_to_nhwc_bf16")) { cudaFreeAsync(xs, st); return rc; }
     }

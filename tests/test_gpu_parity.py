@@ -295,3 +295,24 @@ def test_torch_conv_transpose_cross_check():
         ours = P.prepare_layer(k, pad).forward(x)
         theirs = torch.nn.functional.conv_transpose2d(x, k.flip(2, 3), stride=2, padding=n - 1 - pad)
         assert float((ours - theirs).abs().max()) < 1e-12
+
+
+@pytest.mark.parametrize("compute,shape", [("fp32", (9, 3, 17, 13, 5, 2, 4)), ("bf16", (10, 128, 16, 16, 4, 2, 64)),
+                                           ("bf16", (6, 64, 128, 128, 4, 2, 64))])
+def test_batch_sharding_bitwise(compute, shape):
+    """Each rank's shard (parallel.shard_range) reproduces its slice of the 1-GPU output bit
+    for bit, for the direct, K3 and K3b paths: no collective is needed on the hot path."""
+    import torch
+    from paper_2502_20493_b200.parallel import shard_batch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    b, ci, h, w, n, pad, co = shape
+    dt = torch.bfloat16 if compute == "bf16" else torch.float32
+    x = device_unit_floats((b, ci, h, w), 3, dtype=dt)
+    bank = O.gen_kernel_bank(ci, co, n, 4)
+    layer = P.prepare_layer(bank, pad, compute=compute)
+    full = layer.forward(x)
+    for world in (2, 3, 4):
+        parts = [layer.forward(shard_batch(x, world, r).contiguous()) for r in range(world)]
+        joined = torch.cat(parts)
+        assert torch.equal(joined.view(torch.int16 if dt == torch.bfloat16 else torch.int32),
+                           full.view(torch.int16 if dt == torch.bfloat16 else torch.int32))
