@@ -68,7 +68,8 @@ struct segb_layer {
     void *wd[3] = {nullptr, nullptr, nullptr};  // K2 weights per compute dtype (F32, F64, BF16)
     int n2p = 0;
     void *wg = nullptr;  // K3 weights (bf16, class/tap-major, K-major)
-    int c_in_pad = 0;
+    void *wt = nullptr;  // K3 3xTF32 weights: fp32 hi plane followed by the lo plane
+    int c_in_pad = 0, c_out_pad = 0, c_in_pad32 = 0;  // zero-padded GEMM operand extents
 };
 
 // K2 weights for a compute dtype, built by K1 on first use (prepare builds the
@@ -98,11 +99,12 @@ static int ensure_gemm_weights(segb_layer *L, cudaStream_t st) {
     std::lock_guard<std::mutex> g(L->mu);
     if (!L->wg) {
         L->c_in_pad = (int)ceil_div(L->c_in, 64) * 64;
-        const size_t bytes = 2ull * L->n * L->n * L->c_out * L->c_in_pad;
+        L->c_out_pad = (int)ceil_div(L->c_out, 32) * 32;
+        const size_t bytes = 2ull * L->n * L->n * L->c_out_pad * L->c_in_pad;
         void *p = nullptr;
         cudaError_t e = cudaMalloc(&p, bytes);
         if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-        if (int rc = run_prep_gemm(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->n, p, st)) {
+        if (int rc = run_prep_gemm(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->c_out_pad, L->n, p, st)) {
             cudaFree(p);
             return rc;
         }
@@ -111,12 +113,32 @@ static int ensure_gemm_weights(segb_layer *L, cudaStream_t st) {
     return SEGB_OK;
 }
 
+static int ensure_tf32_weights(segb_layer *L, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(L->mu);
+    if (!L->wt) {
+        L->c_in_pad32 = (int)ceil_div(L->c_in, 32) * 32;
+        L->c_out_pad = (int)ceil_div(L->c_out, 32) * 32;
+        const size_t plane = (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad32;
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, 2 * 4 * plane);
+        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", 8 * plane, cudaGetErrorString(e));
+        if (int rc = run_prep_gemm_tf32(L->bank, L->bank_dtype, L->c_in, L->c_in_pad32, L->c_out, L->c_out_pad, L->n,
+                                        p, (char *)p + 4 * plane, st)) {
+            cudaFree(p);
+            return rc;
+        }
+        L->wt = p;
+    }
+    return SEGB_OK;
+}
+
+// tensor cores for bf16 (kind::f16) and for fp32 as 3xTF32 (kind::tf32)
 static bool igemm_ok(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int compute,
                      int y_dtype) {
-    if (L->engine != SEGB_ENGINE_SEGREGATED || compute != SEGB_BF16) return false;
+    if (L->engine != SEGB_ENGINE_SEGREGATED || (compute != SEGB_BF16 && compute != SEGB_F32)) return false;
     IgemmShape s{};
     s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
-    s.x_dtype = x_dtype; s.y_dtype = y_dtype;
+    s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.compute = compute;
     return igemm_supported(s);
 }
 
@@ -207,6 +229,9 @@ int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int n, i
     int rc = ensure_direct_weights(L, compute, st, &dummy);
     if (!rc && compute == SEGB_BF16 && engine == SEGB_ENGINE_SEGREGATED && igemm_available())
         rc = ensure_gemm_weights(L, st);
+    if (!rc && compute == SEGB_F32 && engine == SEGB_ENGINE_SEGREGATED && n % 2 == 0 && c_in >= 32 &&
+        igemm_available())
+        rc = ensure_tf32_weights(L, st);
     if (rc) {
         segb_release(L);
         return rc;
@@ -229,7 +254,8 @@ int segb_layer_info(const segb_layer *L, int *c_in, int *c_out, int *n, int *pad
 int segb_select_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int compute) {
     if (!L) return fail(SEGB_ERR_VALUE, "null layer");
     if (compute < 0) compute = L->compute;
-    return igemm_ok(L, x_dtype, batch, in_h, in_w, compute, SEGB_BF16) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
+    const int y_dtype = compute == SEGB_F32 ? SEGB_F32 : SEGB_BF16;
+    return igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
 }
 
 int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
@@ -249,11 +275,18 @@ int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch
     if (path == SEGB_PATH_IGEMM) {
         if (!igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype))
             return fail(SEGB_ERR_UNSUPPORTED, "implicit-GEMM path not eligible for this layer/shape/dtype");
-        if (int rc = ensure_gemm_weights(L, st)) return rc;
         IgemmShape s{};
         s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
-        s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.c_in_pad = L->c_in_pad;
-        return run_igemm(s, x, L->wg, y, st);
+        s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.compute = compute;
+        if (compute == SEGB_F32) {
+            if (int rc = ensure_tf32_weights(L, st)) return rc;
+            s.c_in_pad32 = L->c_in_pad32; s.c_out_pad = L->c_out_pad;
+            const size_t plane = (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad32;
+            return run_igemm(s, x, L->wt, (const char *)L->wt + 4 * plane, y, st);
+        }
+        if (int rc = ensure_gemm_weights(L, st)) return rc;
+        s.c_in_pad = L->c_in_pad; s.c_out_pad = L->c_out_pad;
+        return run_igemm(s, x, L->wg, nullptr, y, st);
     }
     if (path != SEGB_PATH_DIRECT) return fail(SEGB_ERR_VALUE, "unknown path %d", path);
     const void *w;
@@ -284,6 +317,7 @@ int segb_release(segb_layer *L) {
     cudaFree(L->bank);
     for (void *p : L->wd) cudaFree(p);
     cudaFree(L->wg);
+    cudaFree(L->wt);
     delete L;
     return SEGB_OK;
 }

@@ -61,96 +61,165 @@ template <> __device__ __forceinline__ void store_y<__nv_bfloat16, float>(__nv_b
     *p = __float2bfloat16_rn(v);
 }
 
-template <typename TX, typename TC, typename TY, bool RBF, int N, int COB, int RQ>
+template <typename TY, typename TC> __device__ __forceinline__ TY cvt_y(TC v);
+template <> __device__ __forceinline__ float cvt_y<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ double cvt_y<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 cvt_y<__nv_bfloat16, float>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename TY, typename TC> __device__ __forceinline__ void store_y2(TY *p, TC a, TC b);
+template <> __device__ __forceinline__ void store_y2<float, float>(float *p, float a, float b) {
+    *reinterpret_cast<float2 *>(p) = make_float2(a, b);
+}
+template <> __device__ __forceinline__ void store_y2<double, double>(double *p, double a, double b) {
+    *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+template <> __device__ __forceinline__ void store_y2<__nv_bfloat16, float>(__nv_bfloat16 *p, float a, float b) {
+    *reinterpret_cast<__nv_bfloat162 *>(p) = __floats2bfloat162_rn(a, b);
+}
+
+// vectorised broadcast read of one (co, ci) tap vector from shared memory
+template <typename TC, int N2P> __device__ __forceinline__ void load_taps(const TC *wp, TC (&wv)[N2P]);
+template <int N2P> __device__ __forceinline__ void load_taps_f(const float *wp, float (&wv)[N2P]) {
+#pragma unroll
+    for (int k = 0; k < N2P; k += 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(wp + k);
+        wv[k] = v.x; wv[k + 1] = v.y; wv[k + 2] = v.z; wv[k + 3] = v.w;
+    }
+}
+template <int N2P> __device__ __forceinline__ void load_taps_d(const double *wp, double (&wv)[N2P]) {
+#pragma unroll
+    for (int k = 0; k < N2P; k += 2) {
+        const double2 v = *reinterpret_cast<const double2 *>(wp + k);
+        wv[k] = v.x; wv[k + 1] = v.y;
+    }
+}
+template <typename TC, int N2P> __device__ __forceinline__ void load_taps(const TC *wp, TC (&wv)[N2P]) {
+    if constexpr (sizeof(TC) == 4) load_taps_f<N2P>(wp, wv);
+    else load_taps_d<N2P>(wp, wv);
+}
+
+template <typename TX, typename TC, typename TY, bool RBF, int N, int COB, int RQ, int CQ>
 __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
-    constexpr int NW = N / 2 + 1;
-    constexpr int WR = RQ + NW - 1;
+    constexpr int NW = N / 2 + 1;          // input rows/cols under one output quad
+    constexpr int WR = RQ + NW - 1;        // window rows for RQ row quads
+    constexpr int WC = CQ + NW - 1;        // window cols for CQ column quads
     constexpr int R0 = (N + 1) / 2, R1 = N / 2;
     constexpr int OFF1 = R0 * R0, OFF2 = R0 * R0 + R0 * R1, OFF3 = R0 * R0 + 2 * R0 * R1;
-    constexpr int N2 = N * N;
+    constexpr int N2P = (N * N + 3) / 4 * 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TC *ws = reinterpret_cast<TC *>(smem_raw);  // [COB][kDirectCiChunk][n2p]
+    TC *ws = reinterpret_cast<TC *>(smem_raw);  // [COB][kDirectCiChunk][N2P]
 
-    const int t = blockIdx.x * 32 + threadIdx.x;
+    const int t0 = (blockIdx.x * 32 + threadIdx.x) * CQ;  // first column quad
     const int nrb = (a.nqr + kDirectRowsPerBlock * RQ - 1) / (kDirectRowsPerBlock * RQ);
     const int q0 = ((blockIdx.y % nrb) * kDirectRowsPerBlock + threadIdx.y) * RQ;
     const int co0 = (blockIdx.y / nrb) * COB;
     const int64_t b = a.b0 + blockIdx.z;
-    const int row0 = q0 - a.swap - a.p, col0 = t - a.swap - a.p;
+    const int row0 = q0 - a.swap - a.p, col0 = t0 - a.swap - a.p;
     const int64_t plane = (int64_t)a.h * a.w_in;
     const TX *xb = reinterpret_cast<const TX *>(a.x) + b * a.c_in * plane;
     const TC *wsrc = reinterpret_cast<const TC *>(a.w);
     const int tid = threadIdx.y * 32 + threadIdx.x;
 
-    TC acc[COB][2 * RQ][2];
+    TC acc[COB][2 * RQ][2 * CQ];
 #pragma unroll
     for (int c = 0; c < COB; ++c)
 #pragma unroll
-        for (int i = 0; i < 2 * RQ; ++i) acc[c][i][0] = acc[c][i][1] = TC(0);
+        for (int i = 0; i < 2 * RQ; ++i)
+#pragma unroll
+            for (int k = 0; k < 2 * CQ; ++k) acc[c][i][k] = TC(0);
 
-    // per-thread validity of each window row / column (bounds of the input)
-    bool rok[WR], cok[NW];
+    // interior warps (the whole window of every lane inside the input) load unpredicated
+    const bool inside = row0 >= 0 && row0 + WR <= a.h && col0 >= 0 && col0 + WC <= a.w_in;
+    const bool warp_inside = __all_sync(0xffffffffu, inside);
+    bool rok[WR], cok[WC];
 #pragma unroll
     for (int i = 0; i < WR; ++i) rok[i] = (unsigned)(row0 + i) < (unsigned)a.h;
 #pragma unroll
-    for (int j = 0; j < NW; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
+    for (int j = 0; j < WC; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
+    const TX *xw = xb + (int64_t)row0 * a.w_in + col0;  // window origin of channel 0 (may point outside)
 
     for (int ci0 = 0; ci0 < a.c_in; ci0 += kDirectCiChunk) {
         const int nci = min(kDirectCiChunk, a.c_in - ci0);
         __syncthreads();
-        for (int i = tid; i < COB * nci * a.n2p; i += 32 * kDirectRowsPerBlock) {
-            const int co = i / (nci * a.n2p);
-            const int rem = i - co * nci * a.n2p;
-            const int ci = rem / a.n2p;
-            const int k = rem - ci * a.n2p;
-            ws[(co * kDirectCiChunk + ci) * a.n2p + k] =
-                (co0 + co < a.c_out) ? wsrc[((int64_t)(co0 + co) * a.c_in + ci0 + ci) * a.n2p + k] : TC(0);
+        for (int i = tid; i < COB * nci * N2P; i += 32 * kDirectRowsPerBlock) {
+            const int co = i / (nci * N2P);
+            const int rem = i - co * nci * N2P;
+            const int ci = rem / N2P;
+            const int k = rem - ci * N2P;
+            ws[(co * kDirectCiChunk + ci) * N2P + k] =
+                (co0 + co < a.c_out) ? wsrc[((int64_t)(co0 + co) * a.c_in + ci0 + ci) * N2P + k] : TC(0);
         }
         __syncthreads();
+#pragma unroll 2
         for (int ci = 0; ci < nci; ++ci) {
-            const TX *xc = xb + (int64_t)(ci0 + ci) * plane;
-            TC win[WR][NW];
+            const TX *xc = xw + (int64_t)(ci0 + ci) * plane;
+            TC win[WR][WC];
+            if (warp_inside) {  // one row pointer per window row, immediate column offsets
 #pragma unroll
-            for (int i = 0; i < WR; ++i)
+                for (int i = 0; i < WR; ++i) {
+                    const TX *rp = xc + i * a.w_in;
 #pragma unroll
-                for (int j = 0; j < NW; ++j)
-                    win[i][j] = (rok[i] && cok[j])
-                                    ? load_x<TX, TC, RBF>(xc + (int64_t)(row0 + i) * a.w_in + col0 + j)
-                                    : TC(0);
+                    for (int j = 0; j < WC; ++j) win[i][j] = load_x<TX, TC, RBF>(rp + j);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < WR; ++i) {
+                    const TX *rp = xc + i * a.w_in;
+#pragma unroll
+                    for (int j = 0; j < WC; ++j) win[i][j] = (rok[i] && cok[j]) ? load_x<TX, TC, RBF>(rp + j) : TC(0);
+                }
+            }
 #pragma unroll
             for (int c = 0; c < COB; ++c) {
-                const TC *wp = ws + (c * kDirectCiChunk + ci) * a.n2p;
-                TC wv[N2];
+                const TC *wp = ws + (c * kDirectCiChunk + ci) * N2P;
+                TC wv[N2P];
+                load_taps<TC, N2P>(wp, wv);  // 128-bit shared-memory broadcasts
 #pragma unroll
-                for (int k = 0; k < N2; ++k) wv[k] = wp[k];
+                for (int qq = 0; qq < RQ; ++qq)
 #pragma unroll
-                for (int qq = 0; qq < RQ; ++qq) {
+                    for (int cq = 0; cq < CQ; ++cq) {
 #pragma unroll
-                    for (int u = 0; u < R0; ++u) {
+                        for (int u = 0; u < R0; ++u) {
 #pragma unroll
-                        for (int v = 0; v < R0; ++v) acc[c][2 * qq][0] += win[qq + u][v] * wv[u * R0 + v];
+                            for (int v = 0; v < R0; ++v)
+                                acc[c][2 * qq][2 * cq] += win[qq + u][cq + v] * wv[u * R0 + v];
 #pragma unroll
-                        for (int v = 0; v < R1; ++v)
-                            acc[c][2 * qq][1] += win[qq + u][1 + v] * wv[OFF1 + u * R1 + v];
+                            for (int v = 0; v < R1; ++v)
+                                acc[c][2 * qq][2 * cq + 1] += win[qq + u][cq + 1 + v] * wv[OFF1 + u * R1 + v];
+                        }
+#pragma unroll
+                        for (int u = 0; u < R1; ++u) {
+#pragma unroll
+                            for (int v = 0; v < R0; ++v)
+                                acc[c][2 * qq + 1][2 * cq] += win[qq + 1 + u][cq + v] * wv[OFF2 + u * R0 + v];
+#pragma unroll
+                            for (int v = 0; v < R1; ++v)
+                                acc[c][2 * qq + 1][2 * cq + 1] +=
+                                    win[qq + 1 + u][cq + 1 + v] * wv[OFF3 + u * R1 + v];
+                        }
                     }
-#pragma unroll
-                    for (int u = 0; u < R1; ++u) {
-#pragma unroll
-                        for (int v = 0; v < R0; ++v)
-                            acc[c][2 * qq + 1][0] += win[qq + 1 + u][v] * wv[OFF2 + u * R0 + v];
-#pragma unroll
-                        for (int v = 0; v < R1; ++v)
-                            acc[c][2 * qq + 1][1] += win[qq + 1 + u][1 + v] * wv[OFF3 + u * R1 + v];
-                    }
-                }
             }
         }
     }
 
-    // stores: each output written exactly once; the quad positions outside
-    // [0, oh) x [0, ow) (odd dims, the swap shift) are not stored
+    // Stores, staged per warp through shared memory so each warp store instruction writes 32
+    // consecutive outputs of one row (a thread's 2*CQ columns are adjacent, which would
+    // otherwise spread one instruction over 16 sectors). Every output element is written
+    // exactly once; quad positions outside [0, oh) x [0, ow) (odd dims, the swap shift) are
+    // not stored.
+    constexpr int SC = 64 * CQ;  // staged columns per warp row
+    __syncthreads();             // the weight chunk area is reused for staging
+    TY *stg = reinterpret_cast<TY *>(smem_raw) + threadIdx.y * (COB * 2 * RQ * SC);
+#pragma unroll
+    for (int c = 0; c < COB; ++c)
+#pragma unroll
+        for (int i = 0; i < 2 * RQ; ++i)
+#pragma unroll
+            for (int k = 0; k < 2 * CQ; ++k)
+                stg[(c * 2 * RQ + i) * SC + threadIdx.x * 2 * CQ + k] = cvt_y<TY, TC>(acc[c][i][k]);
+    __syncwarp();
     TY *yb = reinterpret_cast<TY *>(a.y);
-    const int y_first = 2 * t - a.swap;
+    const int y0 = 2 * (blockIdx.x * 32 * CQ) - a.swap;  // first output column of the warp
 #pragma unroll
     for (int c = 0; c < COB; ++c) {
         if (co0 + c >= a.c_out) break;
@@ -161,9 +230,10 @@ __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
             if ((unsigned)xo >= (unsigned)a.oh) continue;
             TY *row = yc + (int64_t)xo * a.ow;
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const int yo = y_first + s;
-                if ((unsigned)yo < (unsigned)a.ow) store_y<TY, TC>(row + yo, acc[c][i][s]);
+            for (int m = 0; m < 2 * CQ; ++m) {
+                const int col = m * 32 + threadIdx.x;
+                const int yo = y0 + col;
+                if ((unsigned)yo < (unsigned)a.ow) row[yo] = stg[(c * 2 * RQ + i) * SC + col];
             }
         }
     }
@@ -240,18 +310,23 @@ __global__ void __launch_bounds__(256) reference_engine_kernel(DirectArgs a, int
 template <typename TX, typename TC, typename TY, bool RBF, int N, int COB>
 int launch_direct_n(const DirectArgs &a, cudaStream_t st) {
     constexpr int RQ = (N <= 5) ? 4 : 2;
+    constexpr int CQ = (N <= 5 && COB <= 2 && sizeof(TC) == 4) ? 2 : 1;  // column quads per thread
     dim3 block(32, kDirectRowsPerBlock);
     const int64_t nco_blk = ceil_div(a.c_out, COB);
     const int64_t nrb = ceil_div(a.nqr, kDirectRowsPerBlock * RQ);
-    if (nco_blk * nrb > 65535 || ceil_div(a.nqc, 32) > (1ll << 31) - 1)
+    if (nco_blk * nrb > 65535 || ceil_div(a.nqc, 32 * CQ) > (1ll << 31) - 1)
         return fail(SEGB_ERR_UNSUPPORTED, "output too large for the direct kernel grid");
-    const size_t smem = sizeof(TC) * COB * kDirectCiChunk * a.n2p;
+    const size_t smem = std::max(sizeof(TC) * COB * kDirectCiChunk * a.n2p,
+                                 sizeof(TY) * kDirectRowsPerBlock * COB * 2 * RQ * 64 * CQ);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(direct_kernel<TX, TC, TY, RBF, N, COB, RQ, CQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
     for (int64_t b0 = 0; b0 < a.batch; b0 += 65535) {
         DirectArgs c = a;
         c.b0 = b0;
-        dim3 grid((unsigned)ceil_div(a.nqc, 32), (unsigned)(nco_blk * nrb),
+        dim3 grid((unsigned)ceil_div(a.nqc, 32 * CQ), (unsigned)(nco_blk * nrb),
                   (unsigned)std::min<int64_t>(65535, a.batch - b0));
-        direct_kernel<TX, TC, TY, RBF, N, COB, RQ><<<grid, block, smem, st>>>(c);
+        direct_kernel<TX, TC, TY, RBF, N, COB, RQ, CQ><<<grid, block, smem, st>>>(c);
         note_launch();
         if (int rc = check_launch("direct_kernel")) return rc;
     }

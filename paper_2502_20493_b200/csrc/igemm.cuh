@@ -7,12 +7,13 @@ namespace segb {
 
 struct IgemmShape {
     int64_t batch;
-    int c_in, c_out, h, w, n, pad, x_dtype, y_dtype, c_in_pad;
+    int c_in, c_out, h, w, n, pad, x_dtype, y_dtype, c_in_pad, c_out_pad, c_in_pad32;
+    int compute;  // SEGB_BF16 (kind::f16) or SEGB_F32 (3xTF32, kind::tf32)
 };
 
 bool igemm_available();
 bool igemm_supported(const IgemmShape &s);
-int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st);
+int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, cudaStream_t st);
 
 // K3b: row-streaming variant for wide class grids (igemm_rows_sm100.cu)
 bool igemm_rows_supported(const IgemmShape &s);

@@ -480,8 +480,8 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     auto encode = tensor_map_encoder();
     CUtensorMap tmB, tmY;
     {
-        cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out, (cuuint64_t)s.n * s.n};
-        cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out * s.c_in_pad * 2};
+        cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
+        cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out_pad * s.c_in_pad * 2};
         cuuint32_t box[3] = {64, (cuuint32_t)s.c_out, 1};
         cuuint32_t es[3] = {1, 1, 1};
         CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box, es,

@@ -35,7 +35,13 @@
 namespace segb {
 
 constexpr int kThreads = 192;
-constexpr int kBlockK = 64;  // channels per k-step (128 B of bf16)
+// A k-step covers one 128-B SWIZZLE_128B row of channels: 64 bf16 or 32 fp32 (kind::tf32).
+template <bool TF32X3> constexpr int kstep_channels() { return TF32X3 ? 32 : 64; }
+// 3xTF32 partial-sum depth: the tensor core's fp32 accumulation error grows with the number
+// of accumulate steps (measured on B200: ~0.25 ulp per MMA), so every kTf32Chunk k-steps
+// (96 MMAs) the partial is moved into fp32 registers.
+constexpr int kTf32Chunk = 8;
+constexpr int kTf32MaxN = 128;
 
 struct ClassGeom {
     int R, C;             // sub-kernel rows / cols
@@ -59,19 +65,24 @@ template <> __device__ __forceinline__ float cvt_out<float>(float v) { return v;
 template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 // ---------------------------------------------------------------- the kernel
-template <typename TY>
+// TF32X3: fp32 operands as 3xTF32 (A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, ~fp32 accuracy)
+// on tcgen05.mma.kind::tf32; each stage then holds hi and lo tiles of both operands.
+template <typename TY, bool TF32X3>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_tconv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmAlo, const __grid_constant__ CUtensorMap tmBlo,
                        const IgemmParams prm) {
+    constexpr int KCH = kstep_channels<TF32X3>();
+    constexpr int NOP = TF32X3 ? 2 : 1;  // tiles per operand per stage (hi [, lo])
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B atoms
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = prm.stages;
-    const uint32_t a_bytes = kBlockM * kBlockK * 2;
-    const uint32_t b_bytes = prm.n_tile * kBlockK * 2;
-    uint8_t *sA = smem;
-    uint8_t *sB = smem + S * a_bytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * b_bytes);
+    const uint32_t a_bytes = kBlockM * 128;       // one A tile: 128 rows x 128 B
+    const uint32_t b_bytes = prm.n_tile * 128;    // one B tile: n_tile rows x 128 B
+    uint8_t *sA = smem;                           // [stage][NOP] A tiles
+    uint8_t *sB = smem + S * NOP * a_bytes;       // [stage][NOP] B tiles
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * NOP * b_bytes);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
@@ -92,6 +103,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        if (TF32X3) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmBlo) : "memory");
+        }
     }
     if (warp == 1) {  // TMEM: two accumulator buffers of N fp32 columns
         const uint32_t cols = tmem_cols(N);
@@ -122,11 +137,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int v = 0; v < g.C; ++v)
                         for (int kb = 0; kb < prm.k_cblocks; ++kb) {
                             mbar_wait(&empty[stage], phase ^ 1);
-                            mbar_expect_tx(&full[stage], a_bytes + b_bytes);
-                            tma_load_4d(sA + stage * a_bytes, &tmA, &full[stage], kb * kBlockK,
-                                        j0 + g.base_s + v - prm.p, i0 + g.base_r + u - prm.p, b0);
-                            tma_load_3d(sB + stage * b_bytes, &tmB, &full[stage], kb * kBlockK, nb * N,
-                                        g.tap0 + u * g.C + v);
+                            mbar_expect_tx(&full[stage], NOP * (a_bytes + b_bytes));
+                            const int wa = j0 + g.base_s + v - prm.p, ha = i0 + g.base_r + u - prm.p;
+                            const int tap = g.tap0 + u * g.C + v;
+                            tma_load_4d(sA + stage * NOP * a_bytes, &tmA, &full[stage], kb * KCH, wa, ha, b0);
+                            tma_load_3d(sB + stage * NOP * b_bytes, &tmB, &full[stage], kb * KCH, nb * N, tap);
+                            if (TF32X3) {
+                                tma_load_4d(sA + (stage * NOP + 1) * a_bytes, &tmAlo, &full[stage], kb * KCH, wa, ha, b0);
+                                tma_load_3d(sB + (stage * NOP + 1) * b_bytes, &tmBlo, &full[stage], kb * KCH, nb * N, tap);
+                            }
                             if (++stage == S_) { stage = 0; phase ^= 1; }
                         }
             }
@@ -135,25 +154,89 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // ---------------- MMA issuer
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            const uint32_t idesc = idesc_bf16(N);
+            const uint32_t idesc = TF32X3 ? idesc_tf32(N) : idesc_bf16(N);
             for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
                 const ClassGeom &g = prm.cls[t & 3];
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d = tmem_base + acc * N;
                 const int ksteps = g.R * g.C * prm.k_cblocks;
+                uint32_t d = 0;
                 for (int ks = 0; ks < ksteps; ++ks) {
+                    // 3xTF32 accumulates at most kTf32Chunk k-steps per TMEM partial (the
+                    // epilogue sums partials in fp32 registers, round-to-nearest)
+                    const int kc = TF32X3 ? ks % kTf32Chunk : ks;
+                    if (kc == 0) {
+                        if (ks > 0) {
+                            tc_commit(&tfull[acc]);
+                            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                        }
+                        mbar_wait(&tempty[acc], acc_phase ^ 1);
+                        tc_fence_after();
+                        d = tmem_base + acc * N;
+                    }
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + stage * a_bytes), b0 = smem_u32(sB + stage * b_bytes);
+                    const uint32_t a0 = smem_u32(sA + stage * NOP * a_bytes), b0 = smem_u32(sB + stage * NOP * b_bytes);
 #pragma unroll
-                    for (int kk = 0; kk < kBlockK / 16; ++kk)
-                        tc_mma(d, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, (ks | kk) != 0);
+                    for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of 32 B of K (16 bf16 / 8 tf32) per 128-B row
+                        if (TF32X3) {
+                            const uint64_t ah = desc_k_sw128(a0 + kk * 32), al = desc_k_sw128(a0 + a_bytes + kk * 32);
+                            const uint64_t bh = desc_k_sw128(b0 + kk * 32), bl = desc_k_sw128(b0 + b_bytes + kk * 32);
+                            tc_mma_tf32(d, ah, bh, idesc, (kc | kk) != 0);
+                            tc_mma_tf32(d, ah, bl, idesc, 1);
+                            tc_mma_tf32(d, al, bh, idesc, 1);
+                        } else {
+                            tc_mma(d, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, (ks | kk) != 0);
+                        }
+                    }
                     tc_commit(&empty[stage]);
                     if (++stage == S_) { stage = 0; phase ^= 1; }
                 }
                 tc_commit(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (TF32X3) {  // ---------------- epilogue, 3xTF32: sum the TMEM partials in registers
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int64_t plane = (int64_t)prm.oh * prm.ow;
+        float *y = reinterpret_cast<float *>(prm.y);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
+            const int c = t & 3, rest = t >> 2;
+            const int mb = rest % prm.m_tiles, nb = rest / prm.m_tiles;
+            const ClassGeom &g = prm.cls[c];
+            const int nchunks = (g.R * g.C * prm.k_cblocks + kTf32Chunk - 1) / kTf32Chunk;
+            float racc[kTf32MaxN];
+#pragma unroll
+            for (int k = 0; k < kTf32MaxN; ++k) racc[k] = 0.f;
+            for (int pc = 0; pc < nchunks; ++pc) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+#pragma unroll
+                for (int ch = 0; ch < kTf32MaxN / 32; ++ch) {
+                    if (ch * 32 < N) {
+                        uint32_t v[32];
+                        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * N + ch * 32, v);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) racc[ch * 32 + k] += __uint_as_float(v[k]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            const int64_t pos = (int64_t)mb * kBlockM + m;
+            if (pos < prm.class_positions) {
+                const int64_t per = (int64_t)g.rows * g.cols;
+                const int64_t b = pos / per;
+                const int rem = (int)(pos - b * per);
+                const int x = 2 * (rem / g.cols) + g.st_r, yy = 2 * (rem % g.cols) + g.st_s;
+                float *dst = y + (b * prm.c_out + (int64_t)nb * N) * plane + (int64_t)x * prm.ow + yy;
+                const int co_left = prm.c_out - nb * N;
+#pragma unroll
+                for (int k = 0; k < kTf32MaxN; ++k)
+                    if (k < N && k < co_left) dst[(int64_t)k * plane] = racc[k];
             }
         }
     } else {  // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
@@ -180,8 +263,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * N + ch * 32, v);
                 if (valid) {
+                    const int co_left = prm.c_out - nb * N - ch * 32;  // real channels in this chunk
+                    if (co_left >= 32) {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) dst[(int64_t)(ch * 32 + k) * plane] = cvt_out<TY>(__uint_as_float(v[k]));
+                        for (int k = 0; k < 32; ++k)
+                            dst[(int64_t)(ch * 32 + k) * plane] = cvt_out<TY>(__uint_as_float(v[k]));
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            if (k < co_left) dst[(int64_t)(ch * 32 + k) * plane] = cvt_out<TY>(__uint_as_float(v[k]));
+                    }
                 }
             }
             tc_fence_before();
@@ -277,12 +368,39 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 bool igemm_available() { return true; }
 
+// NCHW fp32 -> NHWC fp32 hi/lo planes for the 3xTF32 A operand (hi = TF32(x), lo = TF32(x - hi)).
+__device__ __forceinline__ float tf32_round(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__global__ void nchw_to_nhwc_tf32x2(const float *__restrict__ x, float *__restrict__ hi, float *__restrict__ lo, int C,
+                                    int HW, int64_t total) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {  // e indexes the NHWC output (coalesced stores)
+        const int c = (int)(e % C);
+        const int64_t bhw = e / C;
+        const int64_t b = bhw / HW, hw = bhw % HW;
+        const float v = __ldg(x + (b * C + c) * HW + hw);
+        const float h = tf32_round(v);
+        hi[e] = h;
+        lo[e] = tf32_round(v - h);
+    }
+}
+
 static bool make_params(const IgemmShape &s, IgemmParams &prm) {
-    if (s.n % 2 != 0) return false;               // all four classes share one grid
-    if (s.c_in < 64 || s.c_in % 8 != 0) return false;
-    if (s.c_out % 16 != 0) return false;
-    if (s.x_dtype != SEGB_BF16 && s.x_dtype != SEGB_F32) return false;
-    if (s.y_dtype != SEGB_BF16 && s.y_dtype != SEGB_F32) return false;
+    const bool tf32 = s.compute == SEGB_F32;
+    if (s.n % 2 != 0) return false;  // all four classes share one grid
+    if (tf32) {
+        if (s.c_in < 32 || s.c_in % 4 != 0) return false;
+        if (s.c_out < 16) return false;  // >2x padded N x 3 passes: the FFMA direct kernel is faster
+        if (s.x_dtype != SEGB_F32 || s.y_dtype != SEGB_F32) return false;
+    } else {
+        if (s.c_in < 64 || s.c_in % 8 != 0) return false;
+        if (s.x_dtype != SEGB_BF16 && s.x_dtype != SEGB_F32) return false;
+        if (s.y_dtype != SEGB_BF16 && s.y_dtype != SEGB_F32) return false;
+    }
+    const int cop = s.c_out_pad ? s.c_out_pad : (int)ceil_div(s.c_out, 32) * 32;
     if (s.batch > 65535) return false;
     const int oh = 2 * s.h + 2 * s.pad - s.n, ow = 2 * s.w + 2 * s.pad - s.n;
     if (oh < 2 || ow < 2) return false;
@@ -322,29 +440,33 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
         }
     }
     if (prm.box_b > 256 || prm.box_h > 256 || prm.box_w > 256) return false;
-    int nt = s.c_out <= 256 ? s.c_out : 0;
+    // N tile over the zero-padded output channels (multiple of 32: the epilogue reads
+    // 32-column TMEM chunks); padded channels are computed on zeros and never stored.
+    // 3xTF32 stages hold hi and lo tiles of both operands, so its N tile is capped at 128.
+    const int nmax = tf32 ? 128 : 256;
+    int nt = cop <= nmax ? cop : 0;
     if (!nt)
-        for (int cand : {256, 128, 64, 32, 16})
-            if (s.c_out % cand == 0) { nt = cand; break; }
-    if (nt % 16 || nt > 256) return false;
-    if (nt % 32) return false;  // epilogue reads 32-column chunks
+        for (int cand : {256, 128, 64, 32})
+            if (cand <= nmax && cop % cand == 0) { nt = cand; break; }
+    if (nt % 32 || nt > nmax) return false;
     prm.n_tile = nt;
-    prm.n_blocks = s.c_out / nt;
+    prm.n_blocks = cop / nt;
     prm.batch = (int)s.batch; prm.c_in = s.c_in; prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
-    prm.k_cblocks = (s.c_in + kBlockK - 1) / kBlockK;
+    const int kch = tf32 ? 32 : 64;
+    prm.k_cblocks = (s.c_in + kch - 1) / kch;
     prm.class_positions = s.batch * (int64_t)rows * cols;
     prm.m_tiles = (int)ceil_div(prm.class_positions, kBlockM);
     const int64_t total = 4ll * prm.m_tiles * prm.n_blocks;
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
-    const int stage_bytes = kBlockM * kBlockK * 2 + nt * kBlockK * 2;
+    const int stage_bytes = (tf32 ? 2 : 1) * (kBlockM * 128 + nt * 128);
     prm.stages = std::min(8, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
     return prm.stages >= 2;
 }
 
 static bool use_rows(const IgemmShape &s) {
     const char *e = getenv("SEGB200_IGEMM_GENERIC");
-    return !(e && atoi(e)) && igemm_rows_supported(s);
+    return s.compute == SEGB_BF16 && !(e && atoi(e)) && igemm_rows_supported(s);
 }
 
 bool igemm_supported(const IgemmShape &s) {
@@ -352,15 +474,9 @@ bool igemm_supported(const IgemmShape &s) {
     return use_rows(s) || (make_params(s, prm) && tensor_map_encoder() != nullptr);
 }
 
-int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
-    if (use_rows(s)) return run_igemm_rows(s, x, wg, y, st);
-    IgemmParams prm;
-    if (!make_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM: unsupported shape");
-    auto encode = tensor_map_encoder();
-    if (!encode) return fail(SEGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    // stage the channels-last bf16 A operand (stream-ordered workspace from the
-    // device's default pool, which is told to keep its reservation so steady-state
-    // calls never map memory or block the host)
+static void keep_pool_reserved() {
+    // stream-ordered workspace from the device's default pool, which is told to keep its
+    // reservation so steady-state calls never map memory or block the host
     static std::once_flag pool_once[64];
     int cur = 0;
     cudaGetDevice(&cur);
@@ -371,13 +487,36 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaS
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     });
+}
+
+static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const void *ptr, const cuuint64_t *dims,
+                      const cuuint64_t *strides, const cuuint32_t *box, const char *what) {
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = tensor_map_encoder()(m, dt, rank, const_cast<void *>(ptr), dims, strides, box, es,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? SEGB_OK : fail(SEGB_ERR_CUDA, "tensor map %s: error %d", what, (int)r);
+}
+
+int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, cudaStream_t st) {
+    if (use_rows(s)) return run_igemm_rows(s, x, wg, y, st);
+    IgemmParams prm;
+    if (!make_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM: unsupported shape");
+    if (!tensor_map_encoder()) return fail(SEGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const bool tf32 = s.compute == SEGB_F32;
+    keep_pool_reserved();
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
-    void *xs = nullptr;
-    cudaError_t e = cudaMallocAsync(&xs, elems * 2, st);
+    const int esz = tf32 ? 4 : 2;
+    void *xs = nullptr;  // channels-last A operand: bf16, or fp32 hi followed by fp32 lo
+    cudaError_t e = cudaMallocAsync(&xs, elems * esz * (tf32 ? 2 : 1), st);
     if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "workspace: %s", cudaGetErrorString(e));
+    void *xs_lo = tf32 ? (void *)((char *)xs + elems * esz) : nullptr;
     {
         const int hw = s.h * s.w;
-        if (hw % 8 == 0 && s.c_in % 8 == 0) {
+        if (tf32) {
+            const unsigned g = (unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 64);
+            nchw_to_nhwc_tf32x2<<<g, 256, 0, st>>>((const float *)x, (float *)xs, (float *)xs_lo, s.c_in, hw, elems);
+        } else if (hw % 8 == 0 && s.c_in % 8 == 0) {
             dim3 grd((unsigned)ceil_div(hw, 256), (unsigned)ceil_div(s.c_in, 64), (unsigned)s.batch);
             if (s.x_dtype == SEGB_BF16)
                 nchw_to_nhwc_bf16_v8<__nv_bfloat16><<<grd, 256, 0, st>>>((const __nv_bfloat16 *)x,
@@ -393,46 +532,44 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, void *y, cudaS
                 nchw_to_nhwc_bf16<float><<<grd, blk, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw);
         }
         note_launch();
-        if (int rc = check_launch("nchw_to_nhwc_bf16")) { cudaFreeAsync(xs, st); return rc; }
+        if (int rc = check_launch("nchw->nhwc staging")) { cudaFreeAsync(xs, st); return rc; }
     }
-    CUtensorMap tmA, tmB;
-    {
-        cuuint64_t dims[4] = {(cuuint64_t)s.c_in, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.batch};
-        cuuint64_t strides[3] = {(cuuint64_t)s.c_in * 2, (cuuint64_t)s.w * s.c_in * 2,
-                                 (cuuint64_t)s.h * s.w * s.c_in * 2};
-        cuuint32_t box[4] = {(cuuint32_t)kBlockK, (cuuint32_t)prm.box_w, (cuuint32_t)prm.box_h, (cuuint32_t)prm.box_b};
-        cuuint32_t es[4] = {1, 1, 1, 1};
-        CUresult r = encode(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, xs, dims, strides, box, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) { cudaFreeAsync(xs, st); return fail(SEGB_ERR_CUDA, "tensor map A: error %d", (int)r); }
-    }
-    {
-        cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out, (cuuint64_t)s.n * s.n};
-        cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out * s.c_in_pad * 2};
-        cuuint32_t box[3] = {(cuuint32_t)kBlockK, (cuuint32_t)prm.n_tile, 1};
-        cuuint32_t es[3] = {1, 1, 1};
-        CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box,
-                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) { cudaFreeAsync(xs, st); return fail(SEGB_ERR_CUDA, "tensor map B: error %d", (int)r); }
-    }
+    const int kch = tf32 ? 32 : 64;
+    const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const int cin_pad = tf32 ? s.c_in_pad32 : s.c_in_pad;
+    CUtensorMap tmA, tmB, tmAlo, tmBlo;
+    cuuint64_t adims[4] = {(cuuint64_t)s.c_in, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.batch};
+    cuuint64_t astr[3] = {(cuuint64_t)s.c_in * esz, (cuuint64_t)s.w * s.c_in * esz, (cuuint64_t)s.h * s.w * s.c_in * esz};
+    cuuint32_t abox[4] = {(cuuint32_t)kch, (cuuint32_t)prm.box_w, (cuuint32_t)prm.box_h, (cuuint32_t)prm.box_b};
+    cuuint64_t bdims[3] = {(cuuint64_t)cin_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
+    cuuint64_t bstr[2] = {(cuuint64_t)cin_pad * esz, (cuuint64_t)s.c_out_pad * cin_pad * esz};
+    cuuint32_t bbox[3] = {(cuuint32_t)kch, (cuuint32_t)prm.n_tile, 1};
+    int rc = encode_map(&tmA, dt, 4, xs, adims, astr, abox, "A");
+    if (!rc) rc = encode_map(&tmB, dt, 3, wg, bdims, bstr, bbox, "B");
+    if (!rc && tf32) rc = encode_map(&tmAlo, dt, 4, xs_lo, adims, astr, abox, "A lo");
+    if (!rc && tf32) rc = encode_map(&tmBlo, dt, 3, wg_lo, bdims, bstr, bbox, "B lo");
+    if (rc) { cudaFreeAsync(xs, st); return rc; }
+    if (!tf32) { tmAlo = tmA; tmBlo = tmB; }
     prm.y = y;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t stage_bytes = (size_t)kBlockM * kBlockK * 2 + (size_t)prm.n_tile * kBlockK * 2;
+    const size_t stage_bytes = (size_t)(tf32 ? 2 : 1) * ((size_t)kBlockM * 128 + (size_t)prm.n_tile * 128);
     const size_t smem = 1024 + prm.stages * stage_bytes + (2 * prm.stages + 4) * 8 + 16;
     const unsigned grid = (unsigned)std::min<int64_t>(prm.total_tiles, sms);
-    if (s.y_dtype == SEGB_BF16) {
-        cudaFuncSetAttribute(igemm_tconv_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        igemm_tconv_kernel<__nv_bfloat16><<<grid, kThreads, smem, st>>>(tmA, tmB, prm);
+    if (tf32) {
+        cudaFuncSetAttribute(igemm_tconv_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        igemm_tconv_kernel<float, true><<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
+    } else if (s.y_dtype == SEGB_BF16) {
+        cudaFuncSetAttribute(igemm_tconv_kernel<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        igemm_tconv_kernel<__nv_bfloat16, false><<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
     } else {
-        cudaFuncSetAttribute(igemm_tconv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        igemm_tconv_kernel<float><<<grid, kThreads, smem, st>>>(tmA, tmB, prm);
+        cudaFuncSetAttribute(igemm_tconv_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        igemm_tconv_kernel<float, false><<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
     }
     note_launch();
-    int rc = check_launch("igemm_tconv_kernel");
+    rc = check_launch("igemm_tconv_kernel");
     cudaFreeAsync(xs, st);
     return rc;
 }

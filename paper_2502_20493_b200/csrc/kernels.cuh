@@ -9,8 +9,11 @@ namespace segb {
 int run_segregate(const void *kern, int dtype, int64_t count, int n, void *subs, bool merge, cudaStream_t st);
 int run_prep_direct(const void *bank, int bank_dtype, int c_in, int c_out, int n, int n2p, bool packed,
                     int mode, void *dst, cudaStream_t st);
-int run_prep_gemm(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int n, void *dst,
-                  cudaStream_t st);
+int run_prep_gemm(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
+                  void *dst, cudaStream_t st);
+
+int run_prep_gemm_tf32(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
+                       void *hi, void *lo, cudaStream_t st);
 
 // synthetic inputs (synth.cu)
 int run_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, cudaStream_t st);

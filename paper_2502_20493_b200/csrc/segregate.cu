@@ -85,25 +85,57 @@ __global__ void prep_direct_kernel(const TS *__restrict__ bank, void *dst, int c
 }
 
 // Implicit-GEMM layout (K3): per class c and sub-kernel tap (u, v), a K-major
-// [c_out][c_in_pad] bf16 matrix: dst[((tapbase(c) + u*C + v) * c_out + co) * c_in_pad + ci]
-// = bf16(K[ci, co, 2u + r, 2v + s]); tap bases follow the class-packed order.
+// [c_out_pad][c_in_pad] bf16 matrix: dst[((tapbase(c) + u*C + v) * c_out_pad + co) * c_in_pad + ci]
+// = bf16(K[ci, co, 2u + r, 2v + s]); tap bases follow the class-packed order; the padding
+// rows/columns are zero.
 template <typename TS>
 __global__ void prep_gemm_kernel(const TS *__restrict__ bank, __nv_bfloat16 *dst, int c_in, int c_in_pad,
-                                 int c_out, int n) {
-    const int64_t total = (int64_t)n * n * c_out * c_in_pad;
+                                 int c_out, int c_out_pad, int n) {
+    const int64_t total = (int64_t)n * n * c_out_pad * c_in_pad;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int ci = (int)(e % c_in_pad);
         const int64_t rest = e / c_in_pad;
-        const int co = (int)(rest % c_out);
-        const int k = (int)(rest / c_out);  // class-packed tap index
+        const int co = (int)(rest % c_out_pad);
+        const int k = (int)(rest / c_out_pad);  // class-packed tap index
         float v = 0.f;
-        if (ci < c_in) {
+        if (ci < c_in && co < c_out) {
             int i, j;
             unpack_index(n, k, i, j);
             v = (float)to_f64(bank[(((int64_t)ci * c_out + co) * n + i) * n + j]);
         }
         dst[e] = __float2bfloat16_rn(v);
+    }
+}
+
+// 3xTF32 operand split: hi = x rounded to TF32 (10-bit mantissa, round-to-nearest),
+// lo = TF32(x - hi); x ~= hi + lo to ~2^-22 relative.
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// [tap][c_out_pad][c_in_pad] fp32 hi and lo planes for kind::tf32 (see prep_gemm_kernel)
+template <typename TS>
+__global__ void prep_gemm_tf32_kernel(const TS *__restrict__ bank, float *hi, float *lo, int c_in, int c_in_pad,
+                                      int c_out, int c_out_pad, int n) {
+    const int64_t total = (int64_t)n * n * c_out_pad * c_in_pad;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int ci = (int)(e % c_in_pad);
+        const int64_t rest = e / c_in_pad;
+        const int co = (int)(rest % c_out_pad);
+        const int k = (int)(rest / c_out_pad);
+        float v = 0.f;
+        if (ci < c_in && co < c_out) {
+            int i, j;
+            unpack_index(n, k, i, j);
+            v = (float)to_f64(bank[(((int64_t)ci * c_out + co) * n + i) * n + j]);
+        }
+        const float h = tf32_rn(v);
+        hi[e] = h;
+        lo[e] = tf32_rn(v - h);
     }
 }
 
@@ -155,16 +187,16 @@ int run_prep_direct(const void *bank, int bank_dtype, int c_in, int c_out, int n
     return check_launch("prep_direct_kernel");
 }
 
-int run_prep_gemm(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int n, void *dst,
-                  cudaStream_t st) {
-    const int64_t total = (int64_t)n * n * c_out * c_in_pad;
+int run_prep_gemm(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
+                  void *dst, cudaStream_t st) {
+    const int64_t total = (int64_t)n * n * c_out_pad * c_in_pad;
     const unsigned g = grid_for(total);
     __nv_bfloat16 *d = (__nv_bfloat16 *)dst;
     switch (bank_dtype) {
-        case SEGB_F32: prep_gemm_kernel<float><<<g, 256, 0, st>>>((const float *)bank, d, c_in, c_in_pad, c_out, n); break;
-        case SEGB_F64: prep_gemm_kernel<double><<<g, 256, 0, st>>>((const double *)bank, d, c_in, c_in_pad, c_out, n); break;
+        case SEGB_F32: prep_gemm_kernel<float><<<g, 256, 0, st>>>((const float *)bank, d, c_in, c_in_pad, c_out, c_out_pad, n); break;
+        case SEGB_F64: prep_gemm_kernel<double><<<g, 256, 0, st>>>((const double *)bank, d, c_in, c_in_pad, c_out, c_out_pad, n); break;
         case SEGB_BF16:
-            prep_gemm_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16 *)bank, d, c_in, c_in_pad, c_out, n);
+            prep_gemm_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16 *)bank, d, c_in, c_in_pad, c_out, c_out_pad, n);
             break;
         default: return fail(SEGB_ERR_VALUE, "unknown bank dtype %d", bank_dtype);
     }
@@ -172,4 +204,28 @@ int run_prep_gemm(const void *bank, int bank_dtype, int c_in, int c_in_pad, int 
     return check_launch("prep_gemm_kernel");
 }
 
+}  // namespace segb
+
+namespace segb {
+int run_prep_gemm_tf32(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
+                       void *hi, void *lo, cudaStream_t st) {
+    const int64_t total = (int64_t)n * n * c_out_pad * c_in_pad;
+    const unsigned g = grid_for(total);
+    float *h = (float *)hi, *l = (float *)lo;
+    switch (bank_dtype) {
+        case SEGB_F32:
+            prep_gemm_tf32_kernel<float><<<g, 256, 0, st>>>((const float *)bank, h, l, c_in, c_in_pad, c_out, c_out_pad, n);
+            break;
+        case SEGB_F64:
+            prep_gemm_tf32_kernel<double><<<g, 256, 0, st>>>((const double *)bank, h, l, c_in, c_in_pad, c_out, c_out_pad, n);
+            break;
+        case SEGB_BF16:
+            prep_gemm_tf32_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16 *)bank, h, l, c_in, c_in_pad,
+                                                                    c_out, c_out_pad, n);
+            break;
+        default: return fail(SEGB_ERR_VALUE, "unknown bank dtype %d", bank_dtype);
+    }
+    note_launch();
+    return check_launch("prep_gemm_tf32_kernel");
+}
 }  // namespace segb

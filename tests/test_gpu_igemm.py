@@ -30,6 +30,8 @@ CASES = [  # name, h, w, c_in, n, c_out, pad, batch
     ("odd_pad", 16, 16, 64, 2, 32, 1, 2),        # swap rule on the tensor-core path
     ("n6_p3", 8, 8, 64, 6, 96, 3, 4),
     ("n2_p1", 32, 64, 96, 2, 160, 1, 2),
+    ("dcgan_l5_cout3", 32, 32, 128, 4, 3, 2, 2),  # c_out padded to an N=32 tile
+    ("cout48", 16, 16, 64, 4, 48, 2, 2),
 ]
 
 
@@ -141,3 +143,31 @@ def test_igemm_rows_variant(name, h, w, ci, n, co, pad, b, monkeypatch):
         y32 = layer.forward(x, path="direct", out_dtype=torch.float32).cpu().numpy()
     assert O.compare(y32, ref, 1e-4, 1e-5)["passed"], name
     assert O.compare(yb, y32.astype(np.float64), 2 ** -8 + 1e-4, 1e-6 * float(np.abs(ref).max()))["passed"], name
+
+
+TF32_CASES = [  # fp32 layers on tensor cores as 3xTF32 (kind::tf32): the reference's fp32 gate
+    ("ebgan_l2", 4, 4, 2048, 4, 1024, 2, 8),
+    ("ebgan_l5", 32, 32, 256, 4, 128, 2, 2),
+    ("ebgan_l7", 128, 128, 64, 4, 64, 2, 1),
+    ("dcgan_l5", 32, 32, 128, 4, 3, 2, 2),
+    ("odd_pad_n2", 16, 16, 64, 2, 32, 1, 2),
+    ("n6_p3_tail", 8, 8, 40, 6, 96, 3, 4),
+]
+
+
+@pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", TF32_CASES)
+def test_igemm_3xtf32_fp32_tolerance(name, h, w, ci, n, co, pad, b):
+    """fp32 compute on the tensor-core path must still meet rel 1e-5 / abs 1e-6 against the
+    reference's fp32 engine inputs (oracle evaluated in fp64)."""
+    import torch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    x = device_unit_floats((b, ci, h, w), 900 + ci, dtype=torch.float32)
+    bank = O.gen_kernel_bank(ci, co, n, 901 + ci)
+    layer = P.prepare_layer(bank, pad)  # compute = fp32 (the reference's working precision)
+    assert layer.select_path(0, b, h, w) == "igemm", name
+    y = layer.forward(x, path="igemm").cpu().numpy()
+    ref = O.forward_segregated_batch(x.cpu().numpy().astype(np.float64), bank.astype(np.float64), pad)
+    rep = O.compare(y, ref, 1e-5, 1e-6)
+    assert rep["passed"], (name, rep)
+    yd = layer.forward(x, path="direct").cpu().numpy()
+    assert O.compare(yd, ref, 1e-5, 1e-6)["passed"], name
