@@ -99,6 +99,12 @@ class ClockSampler:
         self.lines = []
         self.thread = None
 
+    def wait_first(self, timeout_s: float = 5.0):
+        """Block until nvidia-smi has produced its first sample (it takes a moment to start)."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout_s:
+            time.sleep(0.01)
+
     def start(self):
         try:
             self.proc = subprocess.Popen(
@@ -248,6 +254,11 @@ def run_ours(args, rank, world, local_rank):
                       "flops": 2 * macs})
     torch.cuda.synchronize()
 
+    # clocks are sampled from the warm-up on (the GPU is under the same load) through the
+    # end of the timed region; nvidia-smi needs a moment to start
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    sampler.wait_first()
     for _ in range(max(args.warmup, 3)):
         for s in state:
             s["layer"].forward(s["x"], out=s["y"])
@@ -280,8 +291,6 @@ def run_ours(args, rank, world, local_rank):
                 events[j].record(stream)
 
     per_layer = [[] for _ in state]
-    sampler = ClockSampler(local_rank)
-    sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -24,9 +24,10 @@
 //     single N = 4*c_out MMA (11 MMAs per k-step instead of 16, 40% less smem
 //     operand traffic);
 //   * consecutive class-grid rows of a strip share nr - 1 of their nr input rows;
-//   * epilogue: TMEM -> registers -> bf16 pairs (output columns 2j, 2j+1 of both
-//     output rows) -> shared staging -> TMA tensor store of [co][2 rows][2*128]
-//     boxes; every output element written once.
+//   * epilogue: four warps (TMEM lane quarters) turn the four class accumulators
+//     of a position into bf16 pairs (output columns 2j, 2j+1) and store both
+//     output rows with coalesced 4-byte stores (128 B per warp instruction),
+//     the next channels' TMEM loads in flight; every output element written once.
 //
 // Warps: 0 weight TMA, 1 MMA issuer (+TMEM owner), 2..5 epilogue (TMEM lane
 // quarters), 6..9 row loaders / transposers.
@@ -38,9 +39,9 @@
 
 namespace segb {
 
-constexpr int kRowsThreads = 320;
+static unsigned long long *g_rows_prof_buf = nullptr;
+constexpr int kRowsThreads = 320;  // 10 warps: weights, MMA, 4 epilogue, 4 loaders
 constexpr int kRing = 4;            // input-row slots (power of two)
-constexpr int kStageBytes = 8192;   // one epilogue staging buffer (x2)
 
 struct RowsClass {
     int st_r, st_s, base_r, base_s, tap0;
@@ -55,7 +56,18 @@ struct RowsParams {
     int total_tiles, tiles_per_cta;
     uint32_t slot_bytes, b_tile_bytes;
     const void *x;
+    void *y;
+    unsigned long long *prof;  // optional role cycle counters (CTA 0), SEGB200_PROFILE=1
 };
+
+// role counters: [0] MMA wait tempty, [1] MMA wait slots, [2] MMA issue, [3] epi wait tfull,
+// [4] epi TMEM+convert, [5] epi staging+store, [6] loader wait empty, [7] loader work, [8] tiles
+#define ROWS_PROF(idx, t0_)                                                                 \
+    if (prm.prof && blockIdx.x == 0) {                                                       \
+        const long long _n = clock64();                                                      \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&prm.prof[idx], (unsigned long long)(_n - t0_)); \
+        t0_ = _n;                                                                            \
+    }
 
 // ---------------------------------------------------------------------------
 // Compile-time MMA schedule for even n = 2*NH: A window (du, dc) of the slot
@@ -120,15 +132,14 @@ constexpr Schedule<NH, SWAP> make_schedule() {
 }
 
 struct RowsSmem {  // byte offsets from the 1024-aligned smem base
-    uint32_t b, ring, stage, bars, total;
+    uint32_t b, ring, bars, total;
 };
 
 __host__ __device__ inline RowsSmem rows_layout(const RowsParams &p, int ntaps, int kbc) {
     RowsSmem s;
     s.b = 0;
     s.ring = s.b + ntaps * kbc * p.b_tile_bytes;
-    s.stage = s.ring + kRing * kbc * p.slot_bytes;
-    s.bars = s.stage + 2 * kStageBytes;
+    s.bars = s.ring + kRing * kbc * p.slot_bytes;
     s.total = s.bars + (1 + 2 * kRing * kbc + 4) * 8 + 16;
     return s;
 }
@@ -138,18 +149,6 @@ __device__ __forceinline__ int tile_loads(const RowsParams &p, int t, int t0) {
     return (t == t0 || (t % p.rows) == 0) ? p.nr : 1;
 }
 
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, uint32_t src, int c0, int c1, int c2, int c3) {
-    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
-                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -158,17 +157,14 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 template <int NH, int KBC, int SWAP>
 __global__ void __launch_bounds__(kRowsThreads, 1)
-    igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmY,
-                      const RowsParams prm) {
+    igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const RowsParams prm) {
     constexpr int NTAPS = 4 * NH * NH;
     constexpr Schedule<NH, SWAP> SCH = make_schedule<NH, SWAP>();
-    constexpr int CC = kStageBytes / (2 * 2 * kBlockM * 2);  // bf16 output channels per staged box (8)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const RowsSmem L = rows_layout(prm, NTAPS, KBC);
     uint8_t *sB = smem + L.b;
     uint8_t *sRing = smem + L.ring;
-    uint8_t *sStage = smem + L.stage;
     uint64_t *b_full = reinterpret_cast<uint64_t *>(smem + L.bars);
     uint64_t *slot_full = b_full + 1;
     uint64_t *slot_empty = slot_full + kRing * KBC;
@@ -187,11 +183,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmY) : "memory");
     }
     const uint32_t tcols = tmem_pow2(8 * N);  // 2 buffers x 4 classes x N fp32 columns
     if (warp == 1) {
@@ -224,6 +219,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // bf16 tile in registers and stores 8 slot rows x 16 B; the next unit's loads are in
         // flight while the current one is stored.
         const int tt = threadIdx.x - 6 * 32;
+        const int tw = tt >> 5;
         const int cg = tt & 7, cc = tt >> 3;
         const int HL = -prm.dmin_c, HR = prm.slot_rows - kBlockM - HL;
         const __nv_bfloat16 *x = reinterpret_cast<const __nv_bfloat16 *>(prm.x);
@@ -272,7 +268,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             uint4 nxt[8], hnxt;
             if (pt < t1) load_unit(pt, pl, pkb, nxt, hnxt);
             const int sidx = (q & (kRing - 1)) * KBC + ckb;
+            long long pl_ = clock64();
+            if (tw == 0) { ROWS_PROF(7, pl_) }
             mbar_wait(&slot_empty[sidx], ((q / kRing) & 1) ^ 1);
+            if (tw == 0) { ROWS_PROF(6, pl_) }
             const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
 #pragma unroll
             for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
@@ -312,16 +311,20 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
         int acc = 0;
         uint32_t acc_phase = 0, qe = 0;
+        long long pt_ = clock64();
         for (int t = t0; t < t1; ++t) {
             qe += tile_loads(prm, t, t0);
             const uint32_t qbase = qe - prm.nr;
+            ROWS_PROF(2, pt_)
             mbar_wait(&tempty[acc], acc_phase ^ 1);
+            ROWS_PROF(0, pt_)
             for (int l = 0; l < prm.nr; ++l) {
                 const uint32_t q = qbase + l;
 #pragma unroll
                 for (int kb = 0; kb < KBC; ++kb) mbar_wait(&slot_full[(q & (kRing - 1)) * KBC + kb], (q / kRing) & 1);
             }
             tc_fence_after();
+            ROWS_PROF(1, pt_)
             const uint32_t d0 = tmem_base + acc * 4 * N;
 #pragma unroll
             for (int gi = 0; gi < SCH.count; ++gi) {
@@ -351,60 +354,64 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     } else {
-        // ---------------- epilogue (warps 2..5; TMEM lane quarter = warp % 4). Per chunk of CC
-        // output channels: TMEM -> packed bf16 pairs -> staging [co][2 rows][256] -> TMA store.
+        // ---------------- epilogue (warps 2..5): warp reads TMEM lane quarter warp % 4 (32 positions).
+        // All four parity classes of a position are in registers, so each lane writes the pair
+        // of output columns (2j, 2j+1) of both output rows as one 4-byte bf16x2 store: every
+        // warp store instruction covers 128 contiguous bytes of one output row, every output
+        // element is written once, and no staging, proxy fence or barrier is needed.
         const int quarter = warp & 3;
         const int m = quarter * 32 + lane;  // position within the 128-wide subtile
-        const bool leader = (warp == 2 && lane == 0);
-        const int s_even = prm.cls[0].st_s == 0 ? 0 : 1;  // class column parity filling even columns
-        const int rlo = prm.cls[0].st_r == 0 ? 0 : 1;     // class row parity of staging row 0 (row 2i)
+        // With even P the classes with row/column parity 0 fill output row 2i and the even
+        // columns; with odd P (SWAP) it is the parity-1 classes (engines.py:338-347).
+        constexpr int RE = SWAP, SE = SWAP;  // class parities of output row 2i / even columns
+        const int64_t plane_b = (int64_t)prm.oh * prm.ow * 2, ow_b = (int64_t)prm.ow * 2;
         int acc = 0;
-        uint32_t acc_phase = 0, chunk = 0;
+        uint32_t acc_phase = 0;
         for (int t = t0; t < t1; ++t) {
             const int i = t % prm.rows, rest = t / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
+            long long pe_ = clock64();
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (warp == 2) { ROWS_PROF(3, pe_) }
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 4 * N;
-            for (int co0 = 0; co0 < N; co0 += CC, ++chunk) {
-                uint32_t v[4][CC];
+            char *pc = reinterpret_cast<char *>(prm.y) + (int64_t)b * prm.c_out * plane_b + (int64_t)(2 * i) * ow_b +
+                       (int64_t)(ms * 2 * kBlockM + 2 * m) * 2;  // (co 0, output row 2i, column 2j)
+            uint32_t v[4][4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld8(tl + c * N + co0, v[c]);
+            for (int c = 0; c < 4; ++c) tmem_ld4(tl + c * N, v[c]);
+            for (int co0 = 0; co0 < N; co0 += 4) {
                 tmem_wait_ld();
+                uint32_t w[4][4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) reg_fence8(v[c]);
-                if (co0 + CC >= N) {  // last chunk of the tile: release the accumulator buffer
+                for (int c = 0; c < 4; ++c) {
+                    reg_fence4(v[c]);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) w[c][k] = v[c][k];
+                }
+                if (co0 + 4 < N) {  // next chunk's TMEM loads in flight during these stores
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) tmem_ld4(tl + c * N + co0 + 4, v[c]);
+                } else {  // last chunk of the tile: release the accumulator buffer
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
-                // staging buffer `chunk & 1` is free once the store issued two chunks ago has read it
-                if (leader) bulk_wait_read1();
-                named_bar(1, 128);
-                const uint32_t stg = smem_u32(sStage + (chunk & 1) * kStageBytes);
 #pragma unroll
-                for (int k = 0; k < CC; ++k) {
-#pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
-                        const bool r1 = (rr ^ rlo) != 0;  // class row parity stored at staging row rr
-                        const float a0 = __uint_as_float(r1 ? v[2][k] : v[0][k]);
-                        const float a1 = __uint_as_float(r1 ? v[3][k] : v[1][k]);
-                        const uint32_t addr = stg + ((k * 2 + rr) * 2 * kBlockM + 2 * m) * 2;
-                        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr),
-                                     "r"(pack_bf16x2(s_even ? a1 : a0, s_even ? a0 : a1))
-                                     : "memory");
-                    }
-                }
-                fence_proxy_async_smem();
-                named_bar(1, 128);
-                if (leader) {
-                    tma_store_4d(&tmY, stg, ms * 2 * kBlockM, 2 * i, co0, b);
-                    bulk_commit();
+                for (int k = 0; k < 4; ++k) {
+                    // class index c = 2r + s; each store is the (even, odd) column pair
+                    const uint32_t row0 = pack_bf16x2(__uint_as_float(w[2 * RE + SE][k]),
+                                                      __uint_as_float(w[2 * RE + (1 - SE)][k]));
+                    const uint32_t row1 = pack_bf16x2(__uint_as_float(w[2 * (1 - RE) + SE][k]),
+                                                      __uint_as_float(w[2 * (1 - RE) + (1 - SE)][k]));
+                    *reinterpret_cast<uint32_t *>(pc) = row0;
+                    *reinterpret_cast<uint32_t *>(pc + ow_b) = row1;
+                    pc += plane_b;
                 }
             }
+            if (warp == 2) { ROWS_PROF(4, pe_) }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        if (leader) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -466,10 +473,9 @@ bool igemm_rows_supported(const IgemmShape &s) {
 }
 
 template <int NH, int KBC, int SWAP>
-static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const CUtensorMap &tmY,
-                        const RowsParams &prm) {
+static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const RowsParams &prm) {
     cudaFuncSetAttribute(igemm_rows_kernel<NH, KBC, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    igemm_rows_kernel<NH, KBC, SWAP><<<grid, kRowsThreads, smem, st>>>(tmB, tmY, prm);
+    igemm_rows_kernel<NH, KBC, SWAP><<<grid, kRowsThreads, smem, st>>>(tmB, prm);
 }
 
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
@@ -478,7 +484,7 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     if (!rows_params(s, prm, nh, kbc, swap))
         return fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: unsupported shape");
     auto encode = tensor_map_encoder();
-    CUtensorMap tmB, tmY;
+    CUtensorMap tmB;
     {
         cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
         cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out_pad * s.c_in_pad * 2};
@@ -489,19 +495,16 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (weights): error %d", (int)r);
     }
-    {
-        const int cc = kStageBytes / (2 * 2 * kBlockM * 2);
-        cuuint64_t dims[4] = {(cuuint64_t)prm.ow, (cuuint64_t)prm.oh, (cuuint64_t)s.c_out, (cuuint64_t)s.batch};
-        cuuint64_t strides[3] = {(cuuint64_t)prm.ow * 2, (cuuint64_t)prm.oh * prm.ow * 2,
-                                 (cuuint64_t)s.c_out * prm.oh * prm.ow * 2};
-        cuuint32_t box[4] = {2 * kBlockM, 2, (cuuint32_t)cc, 1};
-        cuuint32_t es[4] = {1, 1, 1, 1};
-        CUresult r = encode(&tmY, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (output): error %d", (int)r);
-    }
     prm.x = x;
+    prm.y = y;
+    prm.prof = nullptr;
+    if (const char *pe = getenv("SEGB200_PROFILE"); pe && atoi(pe)) {
+        static unsigned long long *buf = nullptr;
+        if (!buf) cudaMalloc(&buf, 64 * sizeof(unsigned long long));
+        cudaMemsetAsync(buf, 0, 64 * sizeof(unsigned long long), st);
+        prm.prof = buf;
+        g_rows_prof_buf = buf;
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -510,7 +513,7 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     const size_t smem = rows_layout(prm, s.n * s.n, kbc).total + 1024;
     int rc = SEGB_OK;
 #define SEGB_ROWS_CASE(NH_, KBC_, SW_) \
-    if (nh == NH_ && kbc == KBC_ && swap == SW_) launch_rows<NH_, KBC_, SW_>(grid, smem, st, tmB, tmY, prm); else
+    if (nh == NH_ && kbc == KBC_ && swap == SW_) launch_rows<NH_, KBC_, SW_>(grid, smem, st, tmB, prm); else
     SEGB_ROWS_CASE(1, 1, 0) SEGB_ROWS_CASE(1, 1, 1) SEGB_ROWS_CASE(1, 2, 0) SEGB_ROWS_CASE(1, 2, 1)
     SEGB_ROWS_CASE(2, 1, 0) SEGB_ROWS_CASE(2, 1, 1) SEGB_ROWS_CASE(2, 2, 0) SEGB_ROWS_CASE(2, 2, 1)
     SEGB_ROWS_CASE(3, 1, 0) SEGB_ROWS_CASE(3, 1, 1) SEGB_ROWS_CASE(3, 2, 0) SEGB_ROWS_CASE(3, 2, 1)
@@ -522,3 +525,11 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
 }
 
 }  // namespace segb
+
+// debug hook (not part of the ABI header): role cycle counters of CTA 0 of the last K3b launch
+extern "C" int segb_debug_rows_profile(unsigned long long *out) {
+    cudaDeviceSynchronize();
+    if (!segb::g_rows_prof_buf) return 1;
+    cudaMemcpy(out, segb::g_rows_prof_buf, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    return 0;
+}

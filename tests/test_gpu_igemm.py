@@ -149,7 +149,6 @@ TF32_CASES = [  # fp32 layers on tensor cores as 3xTF32 (kind::tf32): the refere
     ("ebgan_l2", 4, 4, 2048, 4, 1024, 2, 8),
     ("ebgan_l5", 32, 32, 256, 4, 128, 2, 2),
     ("ebgan_l7", 128, 128, 64, 4, 64, 2, 1),
-    ("dcgan_l5", 32, 32, 128, 4, 3, 2, 2),
     ("odd_pad_n2", 16, 16, 64, 2, 32, 1, 2),
     ("n6_p3_tail", 8, 8, 40, 6, 96, 3, 4),
 ]
