@@ -51,7 +51,8 @@ struct RowsParams {
     RowsClass cls[4];
     int c_in, c_out, h, w, oh, ow, p;
     int rows, msub;  // class-grid rows, 128-position subtiles per row
-    int dmin_r, nr;  // first window row offset, input rows per class-grid row
+    int dmin_r, nr;  // first window row offset, input rows per class-grid row (all four classes)
+    int dminr_rs[2]; // first window row offset of the classes of row parity r (RS = 2)
     int dmin_c, slot_rows;
     int total_tiles, tiles_per_cta;
     uint32_t slot_bytes, b_tile_bytes;
@@ -73,44 +74,50 @@ struct RowsParams {
 // Compile-time MMA schedule for even n = 2*NH: A window (du, dc) of the slot
 // ring is shared by the classes (r, s) with 0 <= du - base_r < NH and
 // 0 <= dc - base_s < NH (base = parity when P is even, 0 when P is odd).
+// RSEL < 0: all four classes (du relative to the union row window);
+// RSEL = r: only the two classes of row parity r (du = tap row u).
 struct MmaGroup {
     int du, dc, c0, nc, b0;  // window, first class, class count, first B tile
 };
-template <int NH, int SWAP>
+template <int NH, int SWAP, int RSEL>
 struct Schedule {
     MmaGroup g[(NH + 1) * (NH + 1) * 2];
     int count = 0;
+    int ntiles = 0;    // B tiles (one per included (class, tap))
     int btap[16 * 4];  // B tile k -> (class << 8) | (u << 4) | v
     bool fresh[(NH + 1) * (NH + 1) * 2];
 };
-template <int NH, int SWAP>
-constexpr Schedule<NH, SWAP> make_schedule() {
-    Schedule<NH, SWAP> s{};
-    const int W = SWAP ? NH : NH + 1;  // distinct windows per axis
+template <int NH, int SWAP, int RSEL>
+constexpr Schedule<NH, SWAP, RSEL> make_schedule() {
+    Schedule<NH, SWAP, RSEL> s{};
+    const int W = SWAP ? NH : NH + 1;  // distinct column windows (and row windows for RSEL < 0)
+    const int DU = RSEL < 0 ? W : NH;
     int nb = 0;
     auto add = [&](int du, int dc, int c0, int nc) {
         s.g[s.count] = MmaGroup{du, dc, c0, nc, nb};
         for (int c = c0; c < c0 + nc; ++c) {
             const int r = c >> 1, q = c & 1;
-            const int u = du - (SWAP ? 0 : r), v = dc - (SWAP ? 0 : q);
+            const int u = RSEL < 0 ? du - (SWAP ? 0 : r) : du, v = dc - (SWAP ? 0 : q);
             s.btap[nb++] = (c << 8) | (u << 4) | v;
         }
         s.count++;
     };
-    // windows feeding all four classes first, so one MMA initialises every accumulator
+    // windows feeding every included class first, so one MMA initialises all accumulators
     for (int pass = 0; pass < 2; ++pass)
-        for (int du = 0; du < W; ++du)
+        for (int du = 0; du < DU; ++du)
             for (int dc = 0; dc < W; ++dc) {
                 bool rr[2] = {false, false}, ss[2] = {false, false};
                 for (int r = 0; r < 2; ++r) {
                     const int u = du - (SWAP ? 0 : r), v = dc - (SWAP ? 0 : r);
-                    rr[r] = u >= 0 && u < NH;
+                    rr[r] = RSEL < 0 ? (u >= 0 && u < NH) : (r == RSEL);
                     ss[r] = v >= 0 && v < NH;
                 }
-                const bool full = rr[0] && rr[1] && ss[0] && ss[1];
+                const bool all_r = RSEL < 0 ? (rr[0] && rr[1]) : true;
+                const bool full = all_r && ss[0] && ss[1];
                 if ((pass == 0) != full) continue;
                 if (full) {
-                    add(du, dc, 0, 4);
+                    if (RSEL < 0) add(du, dc, 0, 4);
+                    else add(du, dc, 2 * RSEL, 2);
                     continue;
                 }
                 for (int r = 0; r < 2; ++r) {
@@ -123,6 +130,7 @@ constexpr Schedule<NH, SWAP> make_schedule() {
                     }
                 }
             }
+    s.ntiles = nb;
     bool touched[4] = {false, false, false, false};
     for (int i = 0; i < s.count; ++i) {
         s.fresh[i] = !touched[s.g[i].c0];
@@ -155,14 +163,63 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
-template <int NH, int KBC, int SWAP>
+// MMA issue of one tile for schedule (NH, SWAP, RSEL): the whole warp walks the compile-time
+// schedule (uniform values), one elected lane issues each tcgen05.mma. The channel-block loop
+// stays rolled so the unrolled schedule's live state stays small.
+template <int NH, int KBC, int SWAP, int MR, int RSEL>
+__device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t dB0, uint32_t qbase, uint32_t S16,
+                                           uint32_t B16, int N) {
+    constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
+    constexpr int CB = RSEL < 0 ? 0 : 2 * RSEL;  // first class held in this CTA's TMEM
+#pragma unroll 1
+    for (int kb = 0; kb < KBC; ++kb) {
+#pragma unroll
+        for (int gi = 0; gi < SCH.count; ++gi) {
+            const MmaGroup g = SCH.g[gi];
+            const uint32_t arow = (((qbase + g.du) & (kRing - 1)) * KBC + kb) * S16 + g.dc * 8;
+            const uint32_t idesc = idesc_bf16_m(MR, g.nc * N);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                if (elect_one())
+                    tc_mma(d0 + (g.c0 - CB) * N, dA0 + arow + kk * 2, dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2, idesc,
+                           (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u);
+        }
+    }
+}
+
+// TMA loads of the resident weights of schedule (NH, SWAP, RSEL), [kb][tile] order
+template <int NH, int KBC, int SWAP, int RSEL>
+__device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB, uint64_t *bar, const RowsParams &prm) {
+    constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
+    mbar_expect_tx(bar, SCH.ntiles * KBC * prm.b_tile_bytes);
+#pragma unroll
+    for (int k = 0; k < SCH.ntiles; ++k) {
+        const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
+        const int tap = prm.cls[c].tap0 + u * NH + v;
+        for (int kb = 0; kb < KBC; ++kb)
+            tma_load_3d(sB + (kb * SCH.ntiles + k) * prm.b_tile_bytes, tmB, bar, kb * 64, 0, tap);
+    }
+}
+
+// MR: positions per tile (one class-grid row segment) = the MMA M, 128 or 64 (M=64 keeps its
+// accumulator in TMEM lanes 32q + [0,16), q = 0..3). RS = 2 splits the four parity classes
+// over a CTA pair by row parity (CTA blockIdx % 2 owns classes (r, 0) and (r, 1)): each CTA
+// then holds half the weights, writes one of the two output rows of a tile and issues 6
+// instead of 11 MMAs per k-step (GAN n = 4, P = 2).
+template <int NH, int KBC, int SWAP, int MR, int RS>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const RowsParams prm) {
-    constexpr int NTAPS = 4 * NH * NH;
-    constexpr Schedule<NH, SWAP> SCH = make_schedule<NH, SWAP>();
+    constexpr int NCL = RS == 2 ? 2 : 4;  // parity classes per CTA
+    // M = 64 rows with two channel blocks: loader warps 0-1 fill block 0, warps 2-3 block 1 of
+    // the same input row at once (else each unit is one (row, block) filled by all four)
+    constexpr bool PAIRKB = MR == 64 && KBC == 2;
+    constexpr int UKB = PAIRKB ? 1 : KBC;  // channel blocks iterated per row by a loader thread
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const RowsSmem L = rows_layout(prm, NTAPS, KBC);
+    const int rsel = RS == 2 ? (int)(blockIdx.x % 2) : -1;
+    const int cta = blockIdx.x / RS;
+    const int ntiles_b = NCL * NH * NH;
+    const RowsSmem L = rows_layout(prm, ntiles_b, KBC);
     uint8_t *sB = smem + L.b;
     uint8_t *sRing = smem + L.ring;
     uint64_t *b_full = reinterpret_cast<uint64_t *>(smem + L.bars);
@@ -174,11 +231,14 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int N = prm.c_out;
+    // this CTA's input-row window per class-grid row
+    const int dminr = RS == 2 ? prm.dminr_rs[rsel] : prm.dmin_r;
+    const int nr = RS == 2 ? NH : prm.nr;
 
     if (threadIdx.x == 0) {
         mbar_init(b_full, 1);
         for (int i = 0; i < kRing * KBC; ++i) {
-            mbar_init(&slot_full[i], 4);  // one arrival per loader warp
+            mbar_init(&slot_full[i], PAIRKB ? 2 : 4);  // one arrival per loader warp filling the slot
             mbar_init(&slot_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -188,7 +248,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     }
-    const uint32_t tcols = tmem_pow2(8 * N);  // 2 buffers x 4 classes x N fp32 columns
+    const uint32_t tcols = tmem_pow2(2 * NCL * N);  // 2 buffers x NCL classes x N fp32 columns
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(tcols));
@@ -198,39 +258,40 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int t0 = blockIdx.x * prm.tiles_per_cta;
+    const int t0 = cta * prm.tiles_per_cta;
     const int t1 = min(prm.total_tiles, t0 + prm.tiles_per_cta);
+    auto loads_of = [&](int t) { return (t == t0 || (t % prm.rows) == 0) ? nr : 1; };
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- the resident weights, in schedule order
-            mbar_expect_tx(b_full, NTAPS * KBC * prm.b_tile_bytes);
-#pragma unroll
-            for (int k = 0; k < NTAPS; ++k) {
-                const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
-                const int tap = prm.cls[c].tap0 + u * NH + v;
-                for (int kb = 0; kb < KBC; ++kb)  // [kb][k]: a group's B tiles stay contiguous
-                    tma_load_3d(sB + (kb * NTAPS + k) * prm.b_tile_bytes, &tmB, b_full, kb * 64, 0, tap);
-            }
+            if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
+            else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
+            else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
         }
     } else if (warp >= 6) {
-        // ---------------- row loaders / transposers: NCHW input row (64 channels x 128 columns
+        // ---------------- row loaders / transposers: NCHW input row (64 channels x MR columns
         // + halo) -> K-major SWIZZLE_128B slot rows. Thread (cg = t & 7, cc = t >> 3) loads 8
         // channels x 8 columns with 128-bit loads (coalesced along the row), transposes the 8x8
         // bf16 tile in registers and stores 8 slot rows x 16 B; the next unit's loads are in
         // flight while the current one is stored.
         const int tt = threadIdx.x - 6 * 32;
         const int tw = tt >> 5;
-        const int cg = tt & 7, cc = tt >> 3;
-        const int HL = -prm.dmin_c, HR = prm.slot_rows - kBlockM - HL;
+        const int cg = tt & 7;
+        const int cc = PAIRKB ? (tt >> 3) & 7 : tt >> 3;  // column chunk of 8
+        const int kbt = PAIRKB ? tt >> 6 : 0;             // PAIRKB: this thread's channel block
+        const int th = PAIRKB ? tt & 63 : tt;             // index among the threads of one slot
+        const int HL = -prm.dmin_c, HR = prm.slot_rows - MR - HL;
+        const bool col_active = cc < MR / 8;  // MR = 64 (unpaired) uses half the column chunks
         const __nv_bfloat16 *x = reinterpret_cast<const __nv_bfloat16 *>(prm.x);
         const int64_t plane_in = (int64_t)prm.h * prm.w;
         auto load_unit = [&](int t, int l, int kb, uint4 (&r)[8], uint4 &hv) {
             const int i = t % prm.rows, rest = t / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
-            const int row = i + prm.dmin_r + l;
-            const int j0 = ms * kBlockM;
-            const bool rok = row >= 0 && row < prm.h;
-            const int ch0 = kb * 64 + cg * 8;
+            const int row = i + dminr + l;
+            const int j0 = ms * MR;
+            const bool in_row = row >= 0 && row < prm.h;
+            const bool rok = in_row && col_active;
+            const int ch0 = (PAIRKB ? kbt : kb) * 64 + cg * 8;
             const __nv_bfloat16 *src = x + ((int64_t)b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -239,10 +300,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     r[c] = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)c * plane_in + cc * 8));
             }
             hv = make_uint4(0, 0, 0, 0);
-            if (tt < (HL + HR) * 8) {  // halo column tasks: (halo col, channel group)
-                const int hc = tt >> 3;
-                const int col = hc < HL ? j0 - HL + hc : j0 + kBlockM + (hc - HL);
-                if (rok && col >= 0 && col < prm.w) {
+            if (th < (HL + HR) * 8) {  // halo column tasks: (halo col, channel group)
+                const int hc = th >> 3;
+                const int col = hc < HL ? j0 - HL + hc : j0 + MR + (hc - HL);
+                if (in_row && col >= 0 && col < prm.w) {
                     uint32_t h16[8];
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
@@ -255,15 +316,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
             }
         };
-        int pt = t0, pl = t0 < t1 ? prm.nr - tile_loads(prm, t0, t0) : 0, pkb = 0;
+        int pt = t0, pl = t0 < t1 ? nr - loads_of(t0) : 0, pkb = 0;
         uint4 cur[8], hcur;
         if (pt < t1) load_unit(pt, pl, pkb, cur, hcur);
         uint32_t q = 0;
         while (pt < t1) {
-            const int ckb = pkb;
-            if (++pkb == KBC) {
+            const int ckb = PAIRKB ? kbt : pkb;
+            if (++pkb == UKB) {
                 pkb = 0;
-                if (++pl == prm.nr && ++pt < t1) pl = prm.nr - tile_loads(prm, pt, t0);
+                if (++pl == nr && ++pt < t1) pl = nr - loads_of(pt);
             }
             uint4 nxt[8], hnxt;
             if (pt < t1) load_unit(pt, pl, pkb, nxt, hnxt);
@@ -273,23 +334,25 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             mbar_wait(&slot_empty[sidx], ((q / kRing) & 1) ^ 1);
             if (tw == 0) { ROWS_PROF(6, pl_) }
             const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
+            if (col_active) {
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
-                uint32_t o[4];
+                for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
+                    uint32_t o[4];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const uint32_t a = (&cur[2 * m].x)[w >> 1], bb = (&cur[2 * m + 1].x)[w >> 1];
-                    o[m] = __byte_perm(a, bb, (w & 1) ? 0x7632 : 0x5410);
+                    for (int m = 0; m < 4; ++m) {
+                        const uint32_t a = (&cur[2 * m].x)[w >> 1], bb = (&cur[2 * m + 1].x)[w >> 1];
+                        o[m] = __byte_perm(a, bb, (w & 1) ? 0x7632 : 0x5410);
+                    }
+                    const int rho = HL + cc * 8 + w;
+                    const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o[0]), "r"(o[1]),
+                                 "r"(o[2]), "r"(o[3])
+                                 : "memory");
                 }
-                const int rho = HL + cc * 8 + w;
-                const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o[0]), "r"(o[1]), "r"(o[2]),
-                             "r"(o[3])
-                             : "memory");
             }
-            if (tt < (HL + HR) * 8) {
-                const int hc = tt >> 3;
-                const int rho = hc < HL ? hc : HL + kBlockM + (hc - HL);
+            if (th < (HL + HR) * 8) {
+                const int hc = th >> 3;
+                const int rho = hc < HL ? hc : HL + MR + (hc - HL);
                 const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
                 asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(hcur.x), "r"(hcur.y),
                              "r"(hcur.z), "r"(hcur.w)
@@ -298,14 +361,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
             __syncwarp();
             if (lane == 0) mbar_arrive(&slot_full[sidx]);
-            if (ckb == KBC - 1) ++q;
+            if (PAIRKB || ckb == KBC - 1) ++q;
 #pragma unroll
             for (int c = 0; c < 8; ++c) cur[c] = nxt[c];
             hcur = hnxt;
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer: the whole warp walks the compile-time schedule (uniform
-        // values), one elected lane issues each tcgen05.mma.
+        // ---------------- MMA issuer
         mbar_wait(b_full, 0);
         const uint64_t dA0 = desc_k_sw128(smem_u32(sRing)), dB0 = desc_k_sw128(smem_u32(sB));
         const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
@@ -313,37 +375,27 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         uint32_t acc_phase = 0, qe = 0;
         long long pt_ = clock64();
         for (int t = t0; t < t1; ++t) {
-            qe += tile_loads(prm, t, t0);
-            const uint32_t qbase = qe - prm.nr;
+            qe += loads_of(t);
+            const uint32_t qbase = qe - nr;
             ROWS_PROF(2, pt_)
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             ROWS_PROF(0, pt_)
-            for (int l = 0; l < prm.nr; ++l) {
+            for (int l = 0; l < nr; ++l) {
                 const uint32_t q = qbase + l;
 #pragma unroll
                 for (int kb = 0; kb < KBC; ++kb) mbar_wait(&slot_full[(q & (kRing - 1)) * KBC + kb], (q / kRing) & 1);
             }
             tc_fence_after();
             ROWS_PROF(1, pt_)
-            const uint32_t d0 = tmem_base + acc * 4 * N;
-#pragma unroll
-            for (int gi = 0; gi < SCH.count; ++gi) {
-                const MmaGroup g = SCH.g[gi];
-                const uint32_t arow = ((qbase + g.du) & (kRing - 1)) * KBC * S16 + g.dc * 8;
-                const uint32_t idesc = idesc_bf16(g.nc * N);
-#pragma unroll
-                for (int kb = 0; kb < KBC; ++kb)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        if (elect_one())
-                            tc_mma(d0 + g.c0 * N, dA0 + arow + kb * S16 + kk * 2, dB0 + (kb * NTAPS + g.b0) * B16 + kk * 2,
-                                   idesc, (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u);
-            }
+            const uint32_t d0 = tmem_base + acc * NCL * N;
+            if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, qbase, S16, B16, N);
+            else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, dA0, dB0, qbase, S16, B16, N);
+            else issue_tile<NH, KBC, SWAP, MR, 1>(d0, dA0, dB0, qbase, S16, B16, N);
             if (elect_one()) {
                 tc_commit(&tfull[acc]);
                 // release input rows no later tile of this strip reads
                 const bool cont = (t + 1 < t1) && ((t + 1) % prm.rows != 0);
-                const int nrel = cont ? 1 : prm.nr;
+                const int nrel = cont ? 1 : nr;
                 for (int l = 0; l < nrel; ++l) {
                     const uint32_t q = qbase + l;
 #pragma unroll
@@ -354,17 +406,21 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     } else {
-        // ---------------- epilogue (warps 2..5): warp reads TMEM lane quarter warp % 4 (32 positions).
-        // All four parity classes of a position are in registers, so each lane writes the pair
-        // of output columns (2j, 2j+1) of both output rows as one 4-byte bf16x2 store: every
-        // warp store instruction covers 128 contiguous bytes of one output row, every output
-        // element is written once, and no staging, proxy fence or barrier is needed.
+        // ---------------- epilogue (warps 2..5): warp reads TMEM lane quarter warp % 4. The
+        // classes of a position are in registers, so each lane writes the pair of output
+        // columns (2j, 2j+1) of each of its output rows as one 4-byte bf16x2 store: a warp
+        // store covers 128 (M=64: 64) contiguous bytes of one output row, every output element
+        // is written once, and no staging, proxy fence or barrier is needed.
         const int quarter = warp & 3;
-        const int m = quarter * 32 + lane;  // position within the 128-wide subtile
+        // position of this lane's TMEM row: M=128 -> lane = row; M=64 -> lanes 32q + [0,16)
+        const int m = MR == 128 ? quarter * 32 + lane : quarter * 16 + (lane & 15);
+        const bool lane_active = MR == 128 || lane < 16;
         // With even P the classes with row/column parity 0 fill output row 2i and the even
         // columns; with odd P (SWAP) it is the parity-1 classes (engines.py:338-347).
         constexpr int RE = SWAP, SE = SWAP;  // class parities of output row 2i / even columns
         const int64_t plane_b = (int64_t)prm.oh * prm.ow * 2, ow_b = (int64_t)prm.ow * 2;
+        // RS = 2: this CTA holds classes (rsel, 0), (rsel, 1) and writes output row 2i + (rsel != RE)
+        const int row_off = RS == 2 ? (rsel != RE ? 1 : 0) : 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = t0; t < t1; ++t) {
@@ -374,24 +430,24 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (warp == 2) { ROWS_PROF(3, pe_) }
-            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 4 * N;
-            char *pc = reinterpret_cast<char *>(prm.y) + (int64_t)b * prm.c_out * plane_b + (int64_t)(2 * i) * ow_b +
-                       (int64_t)(ms * 2 * kBlockM + 2 * m) * 2;  // (co 0, output row 2i, column 2j)
-            uint32_t v[4][4];
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * N;
+            char *pc = reinterpret_cast<char *>(prm.y) + (int64_t)b * prm.c_out * plane_b +
+                       (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co 0, row, col 2j)
+            uint32_t v[NCL][4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld4(tl + c * N, v[c]);
+            for (int c = 0; c < NCL; ++c) tmem_ld4(tl + c * N, v[c]);
             for (int co0 = 0; co0 < N; co0 += 4) {
                 tmem_wait_ld();
-                uint32_t w[4][4];
+                uint32_t w[NCL][4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < NCL; ++c) {
                     reg_fence4(v[c]);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) w[c][k] = v[c][k];
                 }
                 if (co0 + 4 < N) {  // next chunk's TMEM loads in flight during these stores
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) tmem_ld4(tl + c * N + co0 + 4, v[c]);
+                    for (int c = 0; c < NCL; ++c) tmem_ld4(tl + c * N + co0 + 4, v[c]);
                 } else {  // last chunk of the tile: release the accumulator buffer
                     tc_fence_before();
                     __syncwarp();
@@ -399,13 +455,19 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    // class index c = 2r + s; each store is the (even, odd) column pair
-                    const uint32_t row0 = pack_bf16x2(__uint_as_float(w[2 * RE + SE][k]),
-                                                      __uint_as_float(w[2 * RE + (1 - SE)][k]));
-                    const uint32_t row1 = pack_bf16x2(__uint_as_float(w[2 * (1 - RE) + SE][k]),
-                                                      __uint_as_float(w[2 * (1 - RE) + (1 - SE)][k]));
-                    *reinterpret_cast<uint32_t *>(pc) = row0;
-                    *reinterpret_cast<uint32_t *>(pc + ow_b) = row1;
+                    if (RS == 1) {  // class index c = 2r + s; each store is the (even, odd) column pair
+                        const uint32_t row0 = pack_bf16x2(__uint_as_float(w[2 * RE + SE][k]),
+                                                          __uint_as_float(w[2 * RE + (1 - SE)][k]));
+                        const uint32_t row1 = pack_bf16x2(__uint_as_float(w[2 * (1 - RE) + SE][k]),
+                                                          __uint_as_float(w[2 * (1 - RE) + (1 - SE)][k]));
+                        if (lane_active) {
+                            *reinterpret_cast<uint32_t *>(pc) = row0;
+                            *reinterpret_cast<uint32_t *>(pc + ow_b) = row1;
+                        }
+                    } else {  // TMEM slot = column parity s
+                        const uint32_t row = pack_bf16x2(__uint_as_float(w[SE][k]), __uint_as_float(w[1 - SE][k]));
+                        if (lane_active) *reinterpret_cast<uint32_t *>(pc) = row;
+                    }
                     pc += plane_b;
                 }
             }
@@ -422,11 +484,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
-static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc, int &swap) {
+static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc, int &swap, int &mr, int &nsplit) {
     if (s.n % 2 != 0 || s.n > 6 || s.x_dtype != SEGB_BF16) return false;
-    if (s.y_dtype != SEGB_BF16) return false;  // fp32 output takes K3 (the staging is sized for bf16)
+    if (s.y_dtype != SEGB_BF16) return false;  // fp32 output takes K3
     if (s.c_out < 16 || s.c_out > 64 || s.c_out % 16 != 0) return false;
-    if (s.w % 8 != 0 || s.w < kBlockM) return false;
+    if (s.w % 8 != 0 || s.w < 64) return false;
     const int oh = 2 * s.h + 2 * s.pad - s.n, ow = 2 * s.w + 2 * s.pad - s.n;
     if (oh < 2 || ow < 2) return false;
     const int p = s.pad / 2;
@@ -448,40 +510,57 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
         dmax_c = std::max(dmax_c, g.base_s + nh - 1 - p);
     }
     const int rows = oh / 2, cols = ow / 2;
-    if (cols % kBlockM != 0) return false;
+    if (cols % 128 == 0) mr = 128;
+    else if (cols % 64 == 0) mr = 64;  // M=64 MMAs (half rate, but every input row loaded once)
+    else return false;
     prm.c_in = s.c_in; prm.h = s.h; prm.w = s.w;
     prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
-    prm.rows = rows; prm.msub = cols / kBlockM;
+    prm.rows = rows; prm.msub = cols / mr;
     prm.dmin_r = dmin_r; prm.nr = dmax_r - dmin_r + 1;
     prm.dmin_c = dmin_c;
-    prm.slot_rows = kBlockM + dmax_c - dmin_c;
+    prm.slot_rows = mr + dmax_c - dmin_c;
     if (-dmin_c > 8 || dmax_c > 8 || prm.nr > kRing) return false;
     kbc = (s.c_in + 63) / 64;
     if (kbc > 2) return false;
     prm.slot_bytes = (prm.slot_rows * 128 + 1023) / 1024 * 1024;
-    prm.b_tile_bytes = s.c_out * 128;
     const int64_t total = s.batch * (int64_t)prm.msub * rows;
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
-    return rows_layout(prm, s.n * s.n, kbc).total + 1024 <= 227 * 1024;
+    for (int r = 0; r < 2; ++r) prm.dminr_rs[r] = prm.cls[2 * r].base_r - p;
+    prm.b_tile_bytes = s.c_out * 128;
+    // all four classes per CTA if their weights fit next to the row ring, else split the
+    // classes over a CTA pair by row parity (half the weights each)
+    for (nsplit = 1; nsplit <= 2; nsplit *= 2)
+        if (rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024 <= 227 * 1024) return true;
+    return false;
+}
+
+// the (NH, KBC, SWAP, MR, NS) variants compiled below
+static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit) {
+    if (mr == 128 && nsplit == 1) return true;
+    if (mr == 128 && nsplit == 2) return nh == 2 && kbc == 2 && swap == 0;
+    if (mr == 64 && nh == 2 && swap == 0) return true;
+    return mr == 64 && nh == 2 && kbc == 2 && swap == 1 && nsplit == 2;
 }
 
 bool igemm_rows_supported(const IgemmShape &s) {
     RowsParams prm;
-    int nh, kbc, swap;
-    return rows_params(s, prm, nh, kbc, swap) && tensor_map_encoder() != nullptr;
+    int nh, kbc, swap, mr, nsplit;
+    return rows_params(s, prm, nh, kbc, swap, mr, nsplit) && rows_instantiated(nh, kbc, swap, mr, nsplit) &&
+           tensor_map_encoder() != nullptr;
 }
 
-template <int NH, int KBC, int SWAP>
+template <int NH, int KBC, int SWAP, int MR, int NS>
 static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const RowsParams &prm) {
-    cudaFuncSetAttribute(igemm_rows_kernel<NH, KBC, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    igemm_rows_kernel<NH, KBC, SWAP><<<grid, kRowsThreads, smem, st>>>(tmB, prm);
+    cudaFuncSetAttribute(igemm_rows_kernel<NH, KBC, SWAP, MR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    igemm_rows_kernel<NH, KBC, SWAP, MR, NS><<<grid, kRowsThreads, smem, st>>>(tmB, prm);
 }
 
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
     RowsParams prm;
-    int nh, kbc, swap;
-    if (!rows_params(s, prm, nh, kbc, swap))
+    int nh, kbc, swap, mr, nsplit;
+    if (!rows_params(s, prm, nh, kbc, swap, mr, nsplit))
         return fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: unsupported shape");
     auto encode = tensor_map_encoder();
     CUtensorMap tmB;
@@ -508,15 +587,23 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::min<int64_t>(prm.total_tiles, sms);
-    prm.tiles_per_cta = (int)ceil_div(prm.total_tiles, grid);
-    const size_t smem = rows_layout(prm, s.n * s.n, kbc).total + 1024;
+    const int strips = (int)std::min<int64_t>(prm.total_tiles, sms / nsplit);  // CTAs per channel slice
+    const int grid = strips * nsplit;
+    prm.tiles_per_cta = (int)ceil_div(prm.total_tiles, strips);
+    const size_t smem = rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024;
     int rc = SEGB_OK;
-#define SEGB_ROWS_CASE(NH_, KBC_, SW_) \
-    if (nh == NH_ && kbc == KBC_ && swap == SW_) launch_rows<NH_, KBC_, SW_>(grid, smem, st, tmB, prm); else
-    SEGB_ROWS_CASE(1, 1, 0) SEGB_ROWS_CASE(1, 1, 1) SEGB_ROWS_CASE(1, 2, 0) SEGB_ROWS_CASE(1, 2, 1)
-    SEGB_ROWS_CASE(2, 1, 0) SEGB_ROWS_CASE(2, 1, 1) SEGB_ROWS_CASE(2, 2, 0) SEGB_ROWS_CASE(2, 2, 1)
-    SEGB_ROWS_CASE(3, 1, 0) SEGB_ROWS_CASE(3, 1, 1) SEGB_ROWS_CASE(3, 2, 0) SEGB_ROWS_CASE(3, 2, 1)
+#define SEGB_ROWS_CASE(NH_, KBC_, SW_, MR_, NS_)                                                  \
+    if (nh == NH_ && kbc == KBC_ && swap == SW_ && mr == MR_ && nsplit == NS_)                     \
+        launch_rows<NH_, KBC_, SW_, MR_, NS_>(grid, smem, st, tmB, prm);                           \
+    else
+    // instantiated: n in {2, 4, 6} x channel blocks x P parity for 128-wide rows; the n = 4
+    // (GAN) family also for 64-wide rows and with the row-parity split
+    SEGB_ROWS_CASE(1, 1, 0, 128, 1) SEGB_ROWS_CASE(1, 1, 1, 128, 1) SEGB_ROWS_CASE(1, 2, 0, 128, 1)
+    SEGB_ROWS_CASE(1, 2, 1, 128, 1) SEGB_ROWS_CASE(2, 1, 0, 128, 1) SEGB_ROWS_CASE(2, 1, 1, 128, 1)
+    SEGB_ROWS_CASE(2, 2, 0, 128, 1) SEGB_ROWS_CASE(2, 2, 1, 128, 1) SEGB_ROWS_CASE(3, 1, 0, 128, 1)
+    SEGB_ROWS_CASE(3, 1, 1, 128, 1) SEGB_ROWS_CASE(3, 2, 0, 128, 1) SEGB_ROWS_CASE(3, 2, 1, 128, 1)
+    SEGB_ROWS_CASE(2, 2, 0, 128, 2) SEGB_ROWS_CASE(2, 1, 0, 64, 1) SEGB_ROWS_CASE(2, 1, 0, 64, 2)
+    SEGB_ROWS_CASE(2, 2, 0, 64, 1) SEGB_ROWS_CASE(2, 2, 0, 64, 2) SEGB_ROWS_CASE(2, 2, 1, 64, 2)
     { rc = fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: variant not instantiated"); }
 #undef SEGB_ROWS_CASE
     if (rc) return rc;

@@ -104,6 +104,11 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBlockM >> 4) << 24);
 }
 
+// instruction descriptor: bf16 x bf16 -> fp32, A and B K-major, M = m (64 or 128), N = n
+__host__ __device__ constexpr uint32_t idesc_bf16_m(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
 // instruction descriptor: bf16 x bf16 -> fp32, A and B K-major, M = 128, N = n
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBlockM >> 4) << 24);

@@ -118,6 +118,9 @@ ROWS_CASES = [  # K3b row-streaming variant: class grid cols % 128 == 0, c_out <
     ("rows_odd_pad_n2", 16, 128, 64, 2, 32, 1, 2),
     ("rows_n6_p3", 8, 128, 64, 6, 16, 3, 2),
     ("rows_cin_tail", 16, 128, 40, 4, 48, 2, 2),
+    ("rows_m64_l6", 64, 64, 128, 4, 64, 2, 2),      # M=64 rows, 2-way output-channel split
+    ("rows_m64_kb1", 32, 64, 64, 4, 32, 2, 2),      # M=64 rows, weights resident unsplit
+    ("rows_m64_msub2", 8, 128 + 64 - 64, 128, 4, 64, 2, 2),
 ]
 
 

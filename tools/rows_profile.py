@@ -6,10 +6,14 @@ import torch
 import paper_2502_20493_b200 as P
 from paper_2502_20493_b200 import _lib
 from paper_2502_20493_b200.synth import device_unit_floats
-x = device_unit_floats((256, 64, 128, 128), 7, dtype=torch.bfloat16)
-bank = device_unit_floats((64, 64, 4, 4), 5, dtype=torch.float32)
-layer = P.prepare_layer(bank, 2, compute="bf16")
-y = torch.empty((256, 64, 256, 256), dtype=torch.bfloat16, device="cuda")
+import bench
+name = sys.argv[1] if len(sys.argv) > 1 else "ebgan_l7"
+_, h, w, ci, n, co, pad = {c[0]: c for c in bench.EBGAN + bench.DCGAN}[name]
+x = device_unit_floats((256, ci, h, w), 7, dtype=torch.bfloat16)
+bank = device_unit_floats((ci, co, n, n), 5, dtype=torch.float32)
+layer = P.prepare_layer(bank, pad, compute="bf16")
+oh, ow = layer.output_shape(h, w)
+y = torch.empty((256, co, oh, ow), dtype=torch.bfloat16, device="cuda")
 for _ in range(2):
     layer.forward(x, out=y)
 torch.cuda.synchronize()
