@@ -62,9 +62,11 @@ def _compile(src: str, force: bool, extra: list[str]) -> str:
     return obj
 
 
-def build(jobs: int | None = None, force: bool = False, verbose_ptxas: bool = False) -> str:
+def build(jobs: int | None = None, force: bool = False, verbose_ptxas: bool = False,
+          defines: list[str] | None = None) -> str:
     os.makedirs(OBJ, exist_ok=True)
     extra = ["-Xptxas", "-v"] if verbose_ptxas else []
+    extra += [f"-D{d}" for d in defines or []]
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(lambda s: _compile(s, force, extra), srcs))
@@ -81,8 +83,10 @@ def main():
     ap.add_argument("-j", type=int, default=None)
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--ptxas-v", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[],
+                    help="extra preprocessor define (experiments, e.g. SEGB_ROWS_ABLATION); use with --force")
     args = ap.parse_args()
-    print(build(args.j, args.force, args.ptxas_v))
+    print(build(args.j, args.force, args.ptxas_v, args.defines))
 
 
 if __name__ == "__main__":

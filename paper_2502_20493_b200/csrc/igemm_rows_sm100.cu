@@ -41,7 +41,7 @@ namespace segb {
 
 static unsigned long long *g_rows_prof_buf = nullptr;
 constexpr int kRowsThreads = 320;  // 10 warps: weights, MMA, 4 epilogue, 4 loaders
-constexpr int kRing = 4;            // input-row slots (power of two)
+constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
 
 struct RowsClass {
     int st_r, st_s, base_r, base_s, tap0;
@@ -56,10 +56,21 @@ struct RowsParams {
     int dmin_c, slot_rows;
     int total_tiles, tiles_per_cta;
     uint32_t slot_bytes, b_tile_bytes;
+    int ring;  // input-row slots in the ring (nr <= ring <= kRingMax)
     const void *x;
     void *y;
     unsigned long long *prof;  // optional role cycle counters (CTA 0), SEGB200_PROFILE=1
+    int ablate;                // SEGB200_ABLATE bits, see ABL()
 };
+
+// Role ablation for bottleneck experiments, compiled in only with -DSEGB_ROWS_ABLATION
+// (SEGB200_ABLATE bit mask: 1 no output stores, 2 no input loads, 4 no MMAs, 8 no TMEM reads,
+// 16 no slot stores, 32 no TMEM handshake, 64 no slot handshake). Results are garbage then.
+#ifdef SEGB_ROWS_ABLATION
+#define ABL(bit) (prm.ablate & (bit))
+#else
+#define ABL(bit) 0
+#endif
 
 // role counters: [0] MMA wait tempty, [1] MMA wait slots, [2] MMA issue, [3] epi wait tfull,
 // [4] epi TMEM+convert, [5] epi staging+store, [6] loader wait empty, [7] loader work, [8] tiles
@@ -147,8 +158,8 @@ __host__ __device__ inline RowsSmem rows_layout(const RowsParams &p, int ntaps, 
     RowsSmem s;
     s.b = 0;
     s.ring = s.b + ntaps * kbc * p.b_tile_bytes;
-    s.bars = s.ring + kRing * kbc * p.slot_bytes;
-    s.total = s.bars + (1 + 2 * kRing * kbc + 4) * 8 + 16;
+    s.bars = s.ring + p.ring * kbc * p.slot_bytes;
+    s.total = s.bars + (1 + 2 * p.ring * kbc + 4) * 8 + 16;
     return s;
 }
 
@@ -158,17 +169,22 @@ __device__ __forceinline__ int tile_loads(const RowsParams &p, int t, int t0) {
 }
 
 
+// epilogue TMEM chunk: 8 fp32 columns per class per tcgen05.ld (c_out is a multiple of 16)
+constexpr int kEpiChunk = 8;
+__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[kEpiChunk]) { tmem_ld8(taddr, v); }
+__device__ __forceinline__ void reg_fence_chunk(uint32_t (&v)[kEpiChunk]) { reg_fence8(v); }
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
 // MMA issue of one tile for schedule (NH, SWAP, RSEL): the whole warp walks the compile-time
-// schedule (uniform values), one elected lane issues each tcgen05.mma. The channel-block loop
+// schedule (uniform values), lane `leader` issues each tcgen05.mma (no per-MMA branch). The channel-block loop
 // stays rolled so the unrolled schedule's live state stays small.
 template <int NH, int KBC, int SWAP, int MR, int RSEL>
-__device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t dB0, uint32_t qbase, uint32_t S16,
-                                           uint32_t B16, int N) {
+__device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t dB0, uint32_t sq, uint32_t ring,
+                                           uint32_t S16, uint32_t B16, int N, uint32_t leader) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
     constexpr int CB = RSEL < 0 ? 0 : 2 * RSEL;  // first class held in this CTA's TMEM
 #pragma unroll 1
@@ -176,13 +192,13 @@ __device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t d
 #pragma unroll
         for (int gi = 0; gi < SCH.count; ++gi) {
             const MmaGroup g = SCH.g[gi];
-            const uint32_t arow = (((qbase + g.du) & (kRing - 1)) * KBC + kb) * S16 + g.dc * 8;
+            const uint32_t sl = sq + g.du >= ring ? sq + g.du - ring : sq + g.du;  // slot of window row du
+            const uint32_t arow = (sl * KBC + kb) * S16 + g.dc * 8;
             const uint32_t idesc = idesc_bf16_m(MR, g.nc * N);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                if (elect_one())
-                    tc_mma(d0 + (g.c0 - CB) * N, dA0 + arow + kk * 2, dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2, idesc,
-                           (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u);
+                tc_mma_pred(d0 + (g.c0 - CB) * N, dA0 + arow + kk * 2, dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2,
+                            idesc, (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
         }
     }
 }
@@ -224,8 +240,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     uint8_t *sRing = smem + L.ring;
     uint64_t *b_full = reinterpret_cast<uint64_t *>(smem + L.bars);
     uint64_t *slot_full = b_full + 1;
-    uint64_t *slot_empty = slot_full + kRing * KBC;
-    uint64_t *tfull = slot_empty + kRing * KBC;
+    const int ring = prm.ring;
+    uint64_t *slot_empty = slot_full + ring * KBC;
+    uint64_t *tfull = slot_empty + ring * KBC;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
@@ -237,7 +254,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(b_full, 1);
-        for (int i = 0; i < kRing * KBC; ++i) {
+        for (int i = 0; i < ring * KBC; ++i) {
             mbar_init(&slot_full[i], PAIRKB ? 2 : 4);  // one arrival per loader warp filling the slot
             mbar_init(&slot_empty[i], 1);
         }
@@ -296,7 +313,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 r[c] = make_uint4(0, 0, 0, 0);
-                if (rok && ch0 + c < prm.c_in)
+                if (rok && ch0 + c < prm.c_in && !(ABL(2)))
                     r[c] = __ldg(reinterpret_cast<const uint4 *>(src + (int64_t)c * plane_in + cc * 8));
             }
             hv = make_uint4(0, 0, 0, 0);
@@ -316,25 +333,34 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
             }
         };
-        int pt = t0, pl = t0 < t1 ? nr - loads_of(t0) : 0, pkb = 0;
-        uint4 cur[8], hcur;
+        // unit cursor (tile, row of its window, channel block); the loads of the next TWO units
+        // are in flight while the current one waits for its slot and is stored
+        auto advance = [&](int &ut, int &ul, int &ukb) {
+            if (++ukb == UKB) {
+                ukb = 0;
+                if (++ul == nr && ++ut < t1) ul = nr - loads_of(ut);
+            }
+        };
+        int pt = t0, pl = t0 < t1 ? nr - loads_of(t0) : 0, pkb = 0;  // current unit
+        uint4 cur[8], hcur, nxt[8], hnxt;
         if (pt < t1) load_unit(pt, pl, pkb, cur, hcur);
+        int nt = pt, nl = pl, nkb = pkb;  // next unit
+        if (nt < t1) advance(nt, nl, nkb);
+        if (nt < t1) load_unit(nt, nl, nkb, nxt, hnxt);
         uint32_t q = 0;
         while (pt < t1) {
             const int ckb = PAIRKB ? kbt : pkb;
-            if (++pkb == UKB) {
-                pkb = 0;
-                if (++pl == nr && ++pt < t1) pl = nr - loads_of(pt);
-            }
-            uint4 nxt[8], hnxt;
-            if (pt < t1) load_unit(pt, pl, pkb, nxt, hnxt);
-            const int sidx = (q & (kRing - 1)) * KBC + ckb;
+            pt = nt; pl = nl; pkb = nkb;  // the unit after this one becomes "next"
+            if (nt < t1) advance(nt, nl, nkb);
+            uint4 nx2[8], hnx2;
+            if (nt < t1) load_unit(nt, nl, nkb, nx2, hnx2);
+            const int sidx = (q % ring) * KBC + ckb;
             long long pl_ = clock64();
             if (tw == 0) { ROWS_PROF(7, pl_) }
-            mbar_wait(&slot_empty[sidx], ((q / kRing) & 1) ^ 1);
+            if (!(ABL(64))) mbar_wait(&slot_empty[sidx], ((q / ring) & 1) ^ 1);
             if (tw == 0) { ROWS_PROF(6, pl_) }
             const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
-            if (col_active) {
+            if (col_active && !(ABL(16))) {
 #pragma unroll
                 for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
                     uint32_t o[4];
@@ -360,17 +386,22 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
             fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
             __syncwarp();
-            if (lane == 0) mbar_arrive(&slot_full[sidx]);
+            if (lane == 0 && !(ABL(64))) mbar_arrive(&slot_full[sidx]);
             if (PAIRKB || ckb == KBC - 1) ++q;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) cur[c] = nxt[c];
+            for (int c = 0; c < 8; ++c) {
+                cur[c] = nxt[c];
+                nxt[c] = nx2[c];
+            }
             hcur = hnxt;
+            hnxt = hnx2;
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
         mbar_wait(b_full, 0);
         const uint64_t dA0 = desc_k_sw128(smem_u32(sRing)), dB0 = desc_k_sw128(smem_u32(sB));
         const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
+        const uint32_t leader = elect_one();
         int acc = 0;
         uint32_t acc_phase = 0, qe = 0;
         long long pt_ = clock64();
@@ -378,28 +409,32 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             qe += loads_of(t);
             const uint32_t qbase = qe - nr;
             ROWS_PROF(2, pt_)
-            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            if (!(ABL(32))) mbar_wait(&tempty[acc], acc_phase ^ 1);
             ROWS_PROF(0, pt_)
             for (int l = 0; l < nr; ++l) {
                 const uint32_t q = qbase + l;
 #pragma unroll
-                for (int kb = 0; kb < KBC; ++kb) mbar_wait(&slot_full[(q & (kRing - 1)) * KBC + kb], (q / kRing) & 1);
+                for (int kb = 0; kb < KBC; ++kb)
+                    if (!(ABL(64))) mbar_wait(&slot_full[(q % ring) * KBC + kb], (q / ring) & 1);
             }
             tc_fence_after();
             ROWS_PROF(1, pt_)
             const uint32_t d0 = tmem_base + acc * NCL * N;
-            if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, qbase, S16, B16, N);
-            else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, dA0, dB0, qbase, S16, B16, N);
-            else issue_tile<NH, KBC, SWAP, MR, 1>(d0, dA0, dB0, qbase, S16, B16, N);
+            const uint32_t sq = qbase % ring;
+            if (ABL(4)) {
+            } else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
+            else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
+            else issue_tile<NH, KBC, SWAP, MR, 1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             if (elect_one()) {
-                tc_commit(&tfull[acc]);
+                if (!(ABL(32))) tc_commit(&tfull[acc]);
                 // release input rows no later tile of this strip reads
                 const bool cont = (t + 1 < t1) && ((t + 1) % prm.rows != 0);
                 const int nrel = cont ? 1 : nr;
                 for (int l = 0; l < nrel; ++l) {
                     const uint32_t q = qbase + l;
 #pragma unroll
-                    for (int kb = 0; kb < KBC; ++kb) tc_commit(&slot_empty[(q & (kRing - 1)) * KBC + kb]);
+                    for (int kb = 0; kb < KBC; ++kb)
+                        if (!(ABL(64))) tc_commit(&slot_empty[(q % ring) * KBC + kb]);
                 }
             }
             __syncwarp();
@@ -427,46 +462,56 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             const int i = t % prm.rows, rest = t / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
             long long pe_ = clock64();
-            mbar_wait(&tfull[acc], acc_phase);
+            if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (warp == 2) { ROWS_PROF(3, pe_) }
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * N;
             char *pc = reinterpret_cast<char *>(prm.y) + (int64_t)b * prm.c_out * plane_b +
                        (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co 0, row, col 2j)
-            uint32_t v[NCL][4];
+            // CH channels per TMEM load per class; the next chunk's loads are in flight while
+            // this chunk is converted and stored
+            constexpr int CH = kEpiChunk;
+            uint32_t v[NCL][CH];
+            if (ABL(8)) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0 && !(ABL(32))) mbar_arrive(&tempty[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                continue;
+            }
 #pragma unroll
-            for (int c = 0; c < NCL; ++c) tmem_ld4(tl + c * N, v[c]);
-            for (int co0 = 0; co0 < N; co0 += 4) {
+            for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * N, v[c]);
+            for (int co0 = 0; co0 < N; co0 += CH) {
                 tmem_wait_ld();
-                uint32_t w[NCL][4];
+                uint32_t w[NCL][CH];
 #pragma unroll
                 for (int c = 0; c < NCL; ++c) {
-                    reg_fence4(v[c]);
+                    reg_fence_chunk(v[c]);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) w[c][k] = v[c][k];
+                    for (int k = 0; k < CH; ++k) w[c][k] = v[c][k];
                 }
-                if (co0 + 4 < N) {  // next chunk's TMEM loads in flight during these stores
+                if (co0 + CH < N) {
 #pragma unroll
-                    for (int c = 0; c < NCL; ++c) tmem_ld4(tl + c * N + co0 + 4, v[c]);
+                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * N + co0 + CH, v[c]);
                 } else {  // last chunk of the tile: release the accumulator buffer
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < CH; ++k) {
                     if (RS == 1) {  // class index c = 2r + s; each store is the (even, odd) column pair
                         const uint32_t row0 = pack_bf16x2(__uint_as_float(w[2 * RE + SE][k]),
                                                           __uint_as_float(w[2 * RE + (1 - SE)][k]));
                         const uint32_t row1 = pack_bf16x2(__uint_as_float(w[2 * (1 - RE) + SE][k]),
                                                           __uint_as_float(w[2 * (1 - RE) + (1 - SE)][k]));
-                        if (lane_active) {
+                        if (lane_active && !(ABL(1))) {
                             *reinterpret_cast<uint32_t *>(pc) = row0;
                             *reinterpret_cast<uint32_t *>(pc + ow_b) = row1;
                         }
                     } else {  // TMEM slot = column parity s
                         const uint32_t row = pack_bf16x2(__uint_as_float(w[SE][k]), __uint_as_float(w[1 - SE][k]));
-                        if (lane_active) *reinterpret_cast<uint32_t *>(pc) = row;
+                        if (lane_active && !(ABL(1))) *reinterpret_cast<uint32_t *>(pc) = row;
                     }
                     pc += plane_b;
                 }
@@ -519,7 +564,7 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     prm.dmin_r = dmin_r; prm.nr = dmax_r - dmin_r + 1;
     prm.dmin_c = dmin_c;
     prm.slot_rows = mr + dmax_c - dmin_c;
-    if (-dmin_c > 8 || dmax_c > 8 || prm.nr > kRing) return false;
+    if (-dmin_c > 8 || dmax_c > 8) return false;
     kbc = (s.c_in + 63) / 64;
     if (kbc > 2) return false;
     prm.slot_bytes = (prm.slot_rows * 128 + 1023) / 1024 * 1024;
@@ -530,8 +575,15 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     prm.b_tile_bytes = s.c_out * 128;
     // all four classes per CTA if their weights fit next to the row ring, else split the
     // classes over a CTA pair by row parity (half the weights each)
-    for (nsplit = 1; nsplit <= 2; nsplit *= 2)
+    // (the ring gets every slot that fits, up to kRingMax: the slots beyond the nr rows of the
+    // current window let the loaders run ahead of the MMAs and hide the handshake latency)
+    for (nsplit = 1; nsplit <= 2; nsplit *= 2) {
+        const int nr_cta = nsplit == 2 ? nh : prm.nr;
+        const int ring_min = std::max(4, nr_cta);
+        for (prm.ring = kRingMax; prm.ring > ring_min; --prm.ring)
+            if (rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024 <= 227 * 1024) break;
         if (rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024 <= 227 * 1024) return true;
+    }
     return false;
 }
 
@@ -577,6 +629,12 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     prm.x = x;
     prm.y = y;
     prm.prof = nullptr;
+    prm.ablate = 0;
+    if (const char *ab = getenv("SEGB200_ABLATE")) prm.ablate = atoi(ab);
+    if (const char *rg = getenv("SEGB200_ROWS_RING")) {  // debug: cap the ring depth
+        const int nr_cta = nsplit == 2 ? nh : prm.nr;
+        prm.ring = std::max(std::min(prm.ring, atoi(rg)), std::max(4, nr_cta));
+    }
     if (const char *pe = getenv("SEGB200_PROFILE"); pe && atoi(pe)) {
         static unsigned long long *buf = nullptr;
         if (!buf) cudaMalloc(&buf, 64 * sizeof(unsigned long long));

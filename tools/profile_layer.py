@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--path", default="auto")
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (no host gaps)")
     a = ap.parse_args()
     cfg = {c[0]: c for c in bench.EBGAN + bench.DCGAN + bench.DATASET + bench.MNIST}[a.layer]
     name, h, w, ci, n, co, pad = cfg
@@ -33,9 +34,17 @@ def main():
     oh, ow = layer.output_shape(h, w)
     y = torch.empty((a.batch, co, oh, ow), dtype=tdt, device="cuda")
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    run = lambda: layer.forward(x, out=y, path=a.path)  # noqa: E731
+    if a.graph:  # replay a captured graph: no host launch gaps inside the timed region
+        run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            layer.forward(x, out=y, path=a.path)
+        run = g.replay
     for i in range(a.iters):
         s.record()
-        layer.forward(x, out=y, path=a.path)
+        run()
         e.record()
         torch.cuda.synchronize()
         print(f"{name} iter {i}: {s.elapsed_time(e):.3f} ms", flush=True)
