@@ -70,6 +70,7 @@ struct segb_layer {
     void *wg = nullptr;  // K3 weights (bf16, class/tap-major, K-major)
     void *wt = nullptr;  // K3 3xTF32 weights: fp32 hi plane followed by the lo plane
     int c_in_pad = 0, c_out_pad = 0, c_in_pad32 = 0;  // zero-padded GEMM operand extents
+    void *wz = nullptr;  // K3c weights (bf16, (kx, ky, co) rows x 64-padded c_in, K-major)
 };
 
 // K2 weights for a compute dtype, built by K1 on first use (prepare builds the
@@ -109,6 +110,23 @@ static int ensure_gemm_weights(segb_layer *L, cudaStream_t st) {
             return rc;
         }
         L->wg = p;
+    }
+    return SEGB_OK;
+}
+
+static int ensure_scatter_weights(segb_layer *L, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(L->mu);
+    if (!L->wz) {
+        const int c_in_pad = (int)ceil_div(L->c_in, 64) * 64;
+        const size_t bytes = 2ull * scatter_weight_rows(L->c_out, L->n) * c_in_pad;
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        if (int rc = run_prep_scatter(L->bank, L->bank_dtype, L->c_in, c_in_pad, L->c_out, L->n, p, st)) {
+            cudaFree(p);
+            return rc;
+        }
+        L->wz = p;
     }
     return SEGB_OK;
 }
@@ -284,6 +302,10 @@ int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch
             const size_t plane = (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad32;
             return run_igemm(s, x, L->wt, (const char *)L->wt + 4 * plane, y, st);
         }
+        if (igemm_scatter_supported(s)) {
+            if (int rc = ensure_scatter_weights(L, st)) return rc;
+            return run_igemm_scatter(s, x, L->wz, y, st);
+        }
         if (int rc = ensure_gemm_weights(L, st)) return rc;
         s.c_in_pad = L->c_in_pad; s.c_out_pad = L->c_out_pad;
         return run_igemm(s, x, L->wg, nullptr, y, st);
@@ -318,6 +340,7 @@ int segb_release(segb_layer *L) {
     for (void *p : L->wd) cudaFree(p);
     cudaFree(L->wg);
     cudaFree(L->wt);
+    cudaFree(L->wz);
     delete L;
     return SEGB_OK;
 }

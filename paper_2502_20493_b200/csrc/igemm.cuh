@@ -15,6 +15,16 @@ bool igemm_available();
 bool igemm_supported(const IgemmShape &s);
 int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, cudaStream_t st);
 
+// K3c: input-stationary scatter GEMM + gather for narrow outputs (igemm_scatter_sm100.cu)
+bool igemm_scatter_supported(const IgemmShape &s);
+int scatter_weight_rows(int c_out, int n);
+int run_prep_scatter(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int n, void *dst,
+                     cudaStream_t st);
+int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *y, cudaStream_t st);
+
+// stream-ordered workspace pool kept reserved across calls (igemm_sm100.cu)
+void keep_pool_reserved();
+
 // K3b: row-streaming variant for wide class grids (igemm_rows_sm100.cu)
 bool igemm_rows_supported(const IgemmShape &s);
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st);

@@ -471,10 +471,10 @@ static bool use_rows(const IgemmShape &s) {
 
 bool igemm_supported(const IgemmShape &s) {
     IgemmParams prm;
-    return use_rows(s) || (make_params(s, prm) && tensor_map_encoder() != nullptr);
+    return igemm_scatter_supported(s) || use_rows(s) || (make_params(s, prm) && tensor_map_encoder() != nullptr);
 }
 
-static void keep_pool_reserved() {
+void keep_pool_reserved() {
     // stream-ordered workspace from the device's default pool, which is told to keep its
     // reservation so steady-state calls never map memory or block the host
     static std::once_flag pool_once[64];

@@ -30,8 +30,14 @@ CASES = [  # name, h, w, c_in, n, c_out, pad, batch
     ("odd_pad", 16, 16, 64, 2, 32, 1, 2),        # swap rule on the tensor-core path
     ("n6_p3", 8, 8, 64, 6, 96, 3, 4),
     ("n2_p1", 32, 64, 96, 2, 160, 1, 2),
-    ("dcgan_l5_cout3", 32, 32, 128, 4, 3, 2, 2),  # c_out padded to an N=32 tile
+    ("dcgan_l5_cout3", 32, 32, 128, 4, 3, 2, 2),  # K3c scatter GEMM (N = 16 taps x 3)
     ("cout48", 16, 16, 64, 4, 48, 2, 2),
+    # K3c (input-stationary scatter GEMM + gather): odd kernels, odd P, tiles that straddle
+    # images and a partial last tile, 1..4 channel blocks, N up to 256
+    ("scatter_n3_p1", 16, 16, 64, 3, 2, 1, 3),
+    ("scatter_n5_p2_tail", 8, 8, 192, 5, 4, 2, 3),
+    ("scatter_n4_p0_n256", 16, 8, 256, 4, 16, 0, 2),
+    ("scatter_n2_p3", 8, 16, 64, 2, 1, 3, 5),
 ]
 
 
@@ -173,3 +179,15 @@ def test_igemm_3xtf32_fp32_tolerance(name, h, w, ci, n, co, pad, b):
     assert rep["passed"], (name, rep)
     yd = layer.forward(x, path="direct").cpu().numpy()
     assert O.compare(yd, ref, 1e-5, 1e-6)["passed"], name
+
+
+def test_scatter_matches_output_stationary_path(monkeypatch):
+    """K3c and the output-stationary K3 GEMM compute the same layer (SEGB200_IGEMM_NOSCATTER)."""
+    import torch
+    h, w, ci, n, co, pad, b = 32, 32, 128, 4, 3, 2, 3
+    x, bank = _inputs(h, w, ci, n, co, b, 77)
+    layer = P.prepare_layer(bank, pad, compute="bf16")
+    ys = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
+    monkeypatch.setenv("SEGB200_IGEMM_NOSCATTER", "1")
+    yk = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
+    assert O.compare(ys, yk.astype(np.float64), 1e-4, 1e-5)["passed"]
