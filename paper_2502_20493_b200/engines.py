@@ -37,6 +37,21 @@ ENGINES = (ENGINE_REFERENCE, ENGINE_SEGREGATED)
 
 COMPUTE_DTYPES = {"fp32": _lib.F32, "fp64": _lib.F64, "bf16": _lib.BF16}
 
+# host-resident batches at least this large are copied in, computed and copied out as an
+# overlapped pipeline of _PIPELINE_CHUNKS batch chunks (PreparedLayer._forward_host_pipelined)
+_PIPELINE_MIN_BYTES = 8 << 20
+_PIPELINE_CHUNKS = 8
+_COPY_STREAMS: dict = {}
+
+
+def _copy_streams(dev):
+    """Per-device H2D and D2H copy streams of the host pipeline (created once)."""
+    key = str(dev)
+    if key not in _COPY_STREAMS:
+        t = _device.torch()
+        _COPY_STREAMS[key] = (t.cuda.Stream(dev), t.cuda.Stream(dev))
+    return _COPY_STREAMS[key]
+
 
 @dataclass(frozen=True)
 class ComparisonReport:
@@ -226,6 +241,13 @@ class PreparedLayer:
         squeeze = x.dim() == 3
         xb = x[None] if squeeze else x
         host_in = not xb.is_cuda
+        if (host_in and xb.shape[0] >= 2 and (out is None or not out.is_cuda)
+                and xb.numel() * xb.element_size() >= _PIPELINE_MIN_BYTES):
+            y = self._forward_host_pipelined(xb, None if out is None else out.view(
+                (xb.shape[0], self.c_out, out_h, out_w)), path, out_dtype, out_h, out_w)
+            if out is not None:
+                return out
+            return y[0] if squeeze else y
         if host_in:
             xb = xb.to(self.device, non_blocking=True)
         elif xb.device != self.device:
@@ -256,6 +278,79 @@ class PreparedLayer:
         if host_in:
             return (d_y[0] if squeeze else d_y).to("cpu")
         return d_y[0] if squeeze else d_y
+
+    def _forward_host_pipelined(self, xh, out_h_t, path, out_dtype, out_h, out_w):
+        """Host (pinned) batch in, host batch out, as a 3-stage pipeline over batch chunks:
+        the H2D copy of chunk k+1 (copy stream), the kernels of chunk k (caller's stream) and
+        the D2H copy of chunk k-1 (second copy stream) overlap, so PCIe runs both directions at
+        once instead of copy-in / compute / copy-out in series. Samples are independent, so
+        the result is bitwise that of one whole-batch call. Ordered after prior work on the
+        caller's current stream, which waits for the last copy before returning; a returned
+        (not `out=`) tensor is complete on return, as `.to("cpu")` would be."""
+        t = _device.torch()
+        dev = self.device
+        main = t.cuda.current_stream(dev)
+        h2d, d2h = _copy_streams(dev)
+        b = int(xh.shape[0])
+        compute = self._compute_for(xh.dtype)
+        dev_in_dt = {"fp64": t.float64, "fp32": t.float32}.get(compute, xh.dtype)
+        if out_dtype is None:
+            out_dtype = (out_h_t.dtype if out_h_t is not None else
+                         (t.bfloat16 if compute == "bf16" and xh.dtype == t.bfloat16 else
+                          (t.float64 if compute == "fp64" else t.float32)))
+        shape = (b, self.c_out, out_h, out_w)
+        returned = out_h_t is None
+        if returned:
+            out_h_t = t.empty(shape, dtype=out_dtype, pin_memory=True)
+        elif tuple(out_h_t.shape) != shape or not out_h_t.is_contiguous():
+            raise ShapeError(f"out must be a contiguous {shape} tensor, got {tuple(out_h_t.shape)}")
+        elif out_h_t.dtype != out_dtype:
+            raise ValueError(f"out dtype {out_h_t.dtype} != {out_dtype}")
+        nchunk = min(b, _PIPELINE_CHUNKS)
+        cs = (b + nchunk - 1) // nchunk
+        spans = [(i, min(b, i + cs)) for i in range(0, b, cs)]
+        xin = [t.empty((cs,) + tuple(xh.shape[1:]), dtype=xh.dtype, device=dev) for _ in range(2)]
+        yout = [t.empty((cs,) + shape[1:], dtype=out_dtype, device=dev) for _ in range(2)]
+        start = t.cuda.Event()
+        start.record(main)
+        h2d.wait_event(start)
+        d2h.wait_event(start)
+        in_free = [None, None]
+        out_free = [None, None]
+        last = None
+        for k, (a, e) in enumerate(spans):
+            slot, n = k % 2, e - a
+            with t.cuda.stream(h2d):
+                if in_free[slot] is not None:
+                    h2d.wait_event(in_free[slot])
+                xin[slot][:n].copy_(xh[a:e], non_blocking=True)
+                in_ready = t.cuda.Event()
+                in_ready.record(h2d)
+            main.wait_event(in_ready)
+            if out_free[slot] is not None:
+                main.wait_event(out_free[slot])
+            xd = xin[slot][:n]
+            if xd.dtype != dev_in_dt:
+                xd = xd.to(dev_in_dt)
+            self._launch(xd, yout[slot][:n], compute, path)
+            done = t.cuda.Event()
+            done.record(main)
+            in_free[slot] = done
+            with t.cuda.stream(d2h):
+                d2h.wait_event(done)
+                out_h_t[a:e].copy_(yout[slot][:n], non_blocking=True)
+                last = t.cuda.Event()
+                last.record(d2h)
+                out_free[slot] = last
+        for buf in xin:
+            buf.record_stream(h2d)
+        for buf in yout:
+            buf.record_stream(d2h)
+        main.wait_event(last)
+        main.wait_event(in_ready)
+        if returned:
+            main.synchronize()
+        return out_h_t
 
     def _launch(self, d_x, d_y, compute: str, path: str) -> None:
         b, _, h, w = d_x.shape

@@ -316,3 +316,28 @@ def test_batch_sharding_bitwise(compute, shape):
         joined = torch.cat(parts)
         assert torch.equal(joined.view(torch.int16 if dt == torch.bfloat16 else torch.int32),
                            full.view(torch.int16 if dt == torch.bfloat16 else torch.int32))
+
+
+@pytest.mark.parametrize("compute,tdt,b,h", [("bf16", "bfloat16", 16, 64), ("bf16", "bfloat16", 7, 128),
+                                              ("fp32", "float32", 5, 128)])
+def test_host_pipeline_bitwise_equals_device_call(compute, tdt, b, h):
+    """Host batches >= 8 MB go through the chunked H2D / compute / D2H pipeline; the result is
+    bitwise that of one device-resident call, with and without out=, pinned or pageable."""
+    import torch
+    dt = getattr(torch, tdt)
+    w = h
+    ci, co, n, pad = 64, 64, 4, 2
+    bank = O.gen_kernel_bank(ci, co, n, 3)
+    layer = P.prepare_layer(bank, pad, compute=compute)
+    g = torch.Generator().manual_seed(b)
+    xh = torch.rand((b, ci, h, w), generator=g).to(dt)
+    assert xh.numel() * xh.element_size() >= 8 << 20  # takes the pipelined path
+    ref = layer.forward(xh.cuda()).cpu()
+    y1 = layer.forward(xh.pin_memory())
+    assert y1.device.type == "cpu" and torch.equal(y1, ref)
+    out = torch.empty_like(ref).pin_memory()
+    y2 = layer.forward(xh.pin_memory(), out=out)
+    torch.cuda.synchronize()
+    assert y2 is out and torch.equal(out, ref)
+    y3 = layer.forward(xh)  # pageable input
+    assert torch.equal(y3, ref)
