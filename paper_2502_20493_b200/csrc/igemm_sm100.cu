@@ -55,6 +55,7 @@ struct IgemmParams {
     ClassGeom cls[4];
     int batch, c_in, c_out, oh, ow, p;
     int n_tile, n_blocks, k_cblocks, m_tiles, total_tiles, stages;
+    int m_pairs;              // PAIR: position blocks per CTA pair (m_tiles rounded up / 2)
     int box_w, box_h, box_b;  // A box (positions): cols x rows x samples = 128
     int64_t class_positions;  // batch * rows * cols (identical for all classes here)
     void *y;
@@ -67,22 +68,35 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(floa
 // ---------------------------------------------------------------- the kernel
 // TF32X3: fp32 operands as 3xTF32 (A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, ~fp32 accuracy)
 // on tcgen05.mma.kind::tf32; each stage then holds hi and lo tiles of both operands.
-template <typename TY, bool TF32X3>
+// PAIR: the grid is made of 2-CTA clusters. The two CTAs of a pair compute adjacent position
+// blocks (2 mbp, 2 mbp + 1) of the same class and output-channel block in lockstep, so they
+// need the same B tile: each loads one half of it and multicasts it to both, halving the
+// weight traffic from L2 per CTA; a stage is refilled only after both CTAs' MMAs released
+// it (each commit arrives on the stage's empty barrier in both CTAs).
+// PM: 0 = single CTA; 1 = PAIR with the B tile multicast; 2 = PAIR as one 2-SM MMA
+// (tcgen05.mma.cta_group::2, M = 256): each CTA holds its 128 A rows and HALF of the B tile
+// (N/2 rows) at the same shared-memory offsets, the leader (rank 0) issues the MMAs for both,
+// each CTA's TMEM receives its own 128 rows x N columns, the TMA loads of both CTAs signal
+// the leader's full barrier, the leader's commits arrive on both CTAs' empty / tfull
+// barriers and both CTAs' epilogue warps arrive on the leader's tempty barrier.
+template <typename TY, bool TF32X3, int PM>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_tconv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmAlo, const __grid_constant__ CUtensorMap tmBlo,
                        const IgemmParams prm) {
     constexpr int KCH = kstep_channels<TF32X3>();
     constexpr int NOP = TF32X3 ? 2 : 1;  // tiles per operand per stage (hi [, lo])
+    constexpr bool PAIR = PM > 0, TWO = PM == 2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B atoms
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = prm.stages;
     const uint32_t a_bytes = kBlockM * 128;       // one A tile: 128 rows x 128 B
     const uint32_t b_bytes = prm.n_tile * 128;    // one B tile: n_tile rows x 128 B
+    const uint32_t b_cta = TWO ? b_bytes / 2 : b_bytes;  // B bytes held per CTA and stage
     uint8_t *sA = smem;                           // [stage][NOP] A tiles
-    uint8_t *sB = smem + S * NOP * a_bytes;       // [stage][NOP] B tiles
-    uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * NOP * b_bytes);
+    uint8_t *sB = smem + S * NOP * a_bytes;       // [stage][NOP] B tiles (TWO: this CTA's half)
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * NOP * b_cta);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
@@ -90,15 +104,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int N = prm.n_tile;
+    const int rank = PAIR ? (int)cluster_ctarank() : 0;
+    // tile iteration: the pair index walks the pair tiles, both CTAs of a pair in lockstep
+    const int t_begin = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int t_step = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    auto decode = [&](int t, int &c, int &mb, int &nb) {
+        c = t & 3;
+        const int rest = t >> 2;
+        if (PAIR) {
+            mb = 2 * (rest % prm.m_pairs) + rank;
+            nb = rest / prm.m_pairs;
+        } else {
+            mb = rest % prm.m_tiles;
+            nb = rest / prm.m_tiles;
+        }
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], PM == 1 ? 2 : 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], TWO ? 8 : 4);  // TWO: the leader's counts both CTAs' epilogues
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -110,25 +139,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 1) {  // TMEM: two accumulator buffers of N fp32 columns
         const uint32_t cols = tmem_cols(N);
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (TWO) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int S_ = S;
+    // an epilogue warp hands a TMEM accumulator buffer back (TWO: to the leader's barrier)
+    auto release_acc = [&](int a) {
+        if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
+        else mbar_arrive(&tempty[a]);
+    };
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
-                const int c = t & 3, rest = t >> 2;
-                const int mb = rest % prm.m_tiles, nb = rest / prm.m_tiles;
+            for (int t = t_begin; t < prm.total_tiles; t += t_step) {
+                int c, mb, nb;
+                decode(t, c, mb, nb);
                 const ClassGeom &g = prm.cls[c];
-                const int64_t P0 = (int64_t)mb * kBlockM;
+                const int64_t P0 = (int64_t)mb * kBlockM;  // past the last block: zero-filled boxes
                 const int64_t per = (int64_t)g.rows * g.cols;
                 const int b0 = (int)(P0 / per);
                 const int rem = (int)(P0 - b0 * per);
@@ -137,25 +180,60 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int v = 0; v < g.C; ++v)
                         for (int kb = 0; kb < prm.k_cblocks; ++kb) {
                             mbar_wait(&empty[stage], phase ^ 1);
-                            mbar_expect_tx(&full[stage], NOP * (a_bytes + b_bytes));
                             const int wa = j0 + g.base_s + v - prm.p, ha = i0 + g.base_r + u - prm.p;
                             const int tap = g.tap0 + u * g.C + v;
+                            if (TWO) {  // own A rows + own half of B, counted on the leader's barrier
+                                const uint32_t fb = mapa_rank(&full[stage], 0);
+                                if (rank == 0) mbar_expect_tx(&full[stage], NOP * 2 * (a_bytes + b_cta));
+                                tma_load_4d_2sm(sA + stage * NOP * a_bytes, &tmA, fb, kb * KCH, wa, ha, b0);
+                                tma_load_3d_2sm(sB + stage * NOP * b_cta, &tmB, fb, kb * KCH, nb * N + rank * (N / 2),
+                                                tap);
+                                if (TF32X3) {
+                                    tma_load_4d_2sm(sA + (stage * NOP + 1) * a_bytes, &tmAlo, fb, kb * KCH, wa, ha, b0);
+                                    tma_load_3d_2sm(sB + (stage * NOP + 1) * b_cta, &tmBlo, fb, kb * KCH,
+                                                    nb * N + rank * (N / 2), tap);
+                                }
+                                if (++stage == S_) { stage = 0; phase ^= 1; }
+                                continue;
+                            }
+                            mbar_expect_tx(&full[stage], NOP * (a_bytes + b_bytes));
                             tma_load_4d(sA + stage * NOP * a_bytes, &tmA, &full[stage], kb * KCH, wa, ha, b0);
-                            tma_load_3d(sB + stage * NOP * b_bytes, &tmB, &full[stage], kb * KCH, nb * N, tap);
-                            if (TF32X3) {
+                            if (TF32X3)
                                 tma_load_4d(sA + (stage * NOP + 1) * a_bytes, &tmAlo, &full[stage], kb * KCH, wa, ha, b0);
-                                tma_load_3d(sB + (stage * NOP + 1) * b_bytes, &tmBlo, &full[stage], kb * KCH, nb * N, tap);
+                            if (PAIR) {  // this CTA's half of the B tile, to both CTAs
+                                const uint32_t half = b_bytes / 2;
+                                tma_load_3d_mc(sB + stage * NOP * b_bytes + rank * half, &tmB, &full[stage], kb * KCH,
+                                               nb * N + rank * (N / 2), tap, 3);
+                                if (TF32X3)
+                                    tma_load_3d_mc(sB + (stage * NOP + 1) * b_bytes + rank * half, &tmBlo, &full[stage],
+                                                   kb * KCH, nb * N + rank * (N / 2), tap, 3);
+                            } else {
+                                tma_load_3d(sB + stage * NOP * b_bytes, &tmB, &full[stage], kb * KCH, nb * N, tap);
+                                if (TF32X3)
+                                    tma_load_3d(sB + (stage * NOP + 1) * b_bytes, &tmBlo, &full[stage], kb * KCH, nb * N, tap);
                             }
                             if (++stage == S_) { stage = 0; phase ^= 1; }
                         }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
+        // ---------------- MMA issuer (TWO: the leader CTA). The whole warp walks the loop and one
+        // elected lane issues (branch-free MMAs keep the descriptor math in uniform registers).
+        if (!(TWO && rank != 0)) {
+            const uint32_t leader = elect_one();
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            const uint32_t idesc = TF32X3 ? idesc_tf32(N) : idesc_bf16(N);
-            for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
+            const uint32_t idesc = TWO ? (TF32X3 ? idesc_tf32(N) : idesc_bf16(N)) + ((uint32_t)(256 - kBlockM) >> 4 << 24)
+                                       : (TF32X3 ? idesc_tf32(N) : idesc_bf16(N));
+            auto commit = [&](uint64_t *bar, bool both) {
+                if (leader) {
+                    if (TWO) tc_commit_2sm_mc(bar, 3);
+                    else if (PAIR && both) tc_commit_mc(bar, 3);
+                    else tc_commit(bar);
+                }
+                __syncwarp();
+            };
+            for (int t = t_begin; t < prm.total_tiles; t += t_step) {
                 const ClassGeom &g = prm.cls[t & 3];
                 const int ksteps = g.R * g.C * prm.k_cblocks;
                 uint32_t d = 0;
@@ -165,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int kc = TF32X3 ? ks % kTf32Chunk : ks;
                     if (kc == 0) {
                         if (ks > 0) {
-                            tc_commit(&tfull[acc]);
+                            commit(&tfull[acc], false);
                             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                         }
                         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -174,23 +252,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + stage * NOP * a_bytes), b0 = smem_u32(sB + stage * NOP * b_bytes);
+                    const uint32_t a0 = smem_u32(sA + stage * NOP * a_bytes), b0 = smem_u32(sB + stage * NOP * b_cta);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of 32 B of K (16 bf16 / 8 tf32) per 128-B row
                         if (TF32X3) {
                             const uint64_t ah = desc_k_sw128(a0 + kk * 32), al = desc_k_sw128(a0 + a_bytes + kk * 32);
-                            const uint64_t bh = desc_k_sw128(b0 + kk * 32), bl = desc_k_sw128(b0 + b_bytes + kk * 32);
-                            tc_mma_tf32(d, ah, bh, idesc, (kc | kk) != 0);
-                            tc_mma_tf32(d, ah, bl, idesc, 1);
-                            tc_mma_tf32(d, al, bh, idesc, 1);
+                            const uint64_t bh = desc_k_sw128(b0 + kk * 32), bl = desc_k_sw128(b0 + b_cta + kk * 32);
+                            tc_mma_any<TWO ? 2 : 1, true>(d, ah, bh, idesc, (kc | kk) != 0, leader);
+                            tc_mma_any<TWO ? 2 : 1, true>(d, ah, bl, idesc, 1, leader);
+                            tc_mma_any<TWO ? 2 : 1, true>(d, al, bh, idesc, 1, leader);
                         } else {
-                            tc_mma(d, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, (ks | kk) != 0);
+                            tc_mma_any<TWO ? 2 : 1, false>(d, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32),
+                                                           idesc, (ks | kk) != 0, leader);
                         }
                     }
-                    tc_commit(&empty[stage]);
+                    commit(&empty[stage], true);
                     if (++stage == S_) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(&tfull[acc]);
+                commit(&tfull[acc], false);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -201,9 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         float *y = reinterpret_cast<float *>(prm.y);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
-            const int c = t & 3, rest = t >> 2;
-            const int mb = rest % prm.m_tiles, nb = rest / prm.m_tiles;
+        for (int t = t_begin; t < prm.total_tiles; t += t_step) {
+            int c, mb, nb;
+            decode(t, c, mb, nb);
             const ClassGeom &g = prm.cls[c];
             const int nchunks = (g.R * g.C * prm.k_cblocks + kTf32Chunk - 1) / kTf32Chunk;
             float racc[kTf32MaxN];
@@ -223,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) release_acc(acc);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
             const int64_t pos = (int64_t)mb * kBlockM + m;
@@ -246,9 +325,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         TY *y = reinterpret_cast<TY *>(prm.y);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < prm.total_tiles; t += gridDim.x) {
-            const int c = t & 3, rest = t >> 2;
-            const int mb = rest % prm.m_tiles, nb = rest / prm.m_tiles;
+        for (int t = t_begin; t < prm.total_tiles; t += t_step) {
+            int c, mb, nb;
+            decode(t, c, mb, nb);
             const ClassGeom &g = prm.cls[c];
             const int64_t pos = (int64_t)mb * kBlockM + m;
             const bool valid = pos < prm.class_positions;
@@ -277,17 +356,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) release_acc(acc);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (TWO) cluster_sync_all();  // the leader's MMAs write this CTA's TMEM until both are done
     if (warp == 1) {
         tc_fence_after();
         const uint32_t cols = tmem_cols(N);
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
+        if (TWO) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
     }
+    if (PAIR) cluster_sync_all();  // the peer may still multicast into / arrive on this CTA
 }
 
 // NCHW (bf16 or fp32) -> NHWC bf16 staging: the channels-last A operand.
@@ -456,6 +538,7 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     prm.k_cblocks = (s.c_in + kch - 1) / kch;
     prm.class_positions = s.batch * (int64_t)rows * cols;
     prm.m_tiles = (int)ceil_div(prm.class_positions, kBlockM);
+    prm.m_pairs = (prm.m_tiles + 1) / 2;
     const int64_t total = 4ll * prm.m_tiles * prm.n_blocks;
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
@@ -496,6 +579,31 @@ static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const vo
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? SEGB_OK : fail(SEGB_ERR_CUDA, "tensor map %s: error %d", what, (int)r);
+}
+
+template <typename TY, bool TF32X3, int PM>
+static int launch_k3(unsigned grid, size_t smem, cudaStream_t st, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                     const CUtensorMap &tmAlo, const CUtensorMap &tmBlo, const IgemmParams &prm) {
+    auto kern = igemm_tconv_kernel<TY, TF32X3, PM>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (PM == 0) {
+        kern<<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
+        return SEGB_OK;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmAlo, tmBlo, prm);
+    return e == cudaSuccess ? SEGB_OK : fail(SEGB_ERR_CUDA, "igemm_tconv_kernel (pair): %s", cudaGetErrorString(e));
 }
 
 int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, cudaStream_t st) {
@@ -543,7 +651,22 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     cuuint32_t abox[4] = {(cuuint32_t)kch, (cuuint32_t)prm.box_w, (cuuint32_t)prm.box_h, (cuuint32_t)prm.box_b};
     cuuint64_t bdims[3] = {(cuuint64_t)cin_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
     cuuint64_t bstr[2] = {(cuuint64_t)cin_pad * esz, (cuuint64_t)s.c_out_pad * cin_pad * esz};
-    cuuint32_t bbox[3] = {(cuuint32_t)kch, (cuuint32_t)prm.n_tile, 1};
+    // CTA pairs: pm = 2 runs two position blocks as one 2-SM MMA (cta_group::2, M = 256, half
+    // of the B tile per CTA: more pipeline stages, half the weight traffic); pm = 1 multicasts B
+    // to two single-SM MMAs. Measured with the branch-free MMA warp (profiles/README.md): pm = 2
+    // is fastest for every GAN layer in bf16 and 3xTF32, so it is the default.
+    // SEGB200_K3_PAIR=0/1/2 overrides (A/B experiments).
+    const char *pm_env = getenv("SEGB200_K3_PAIR");
+    int pm = pm_env ? std::max(0, std::min(2, atoi(pm_env))) : 2;
+    if (prm.m_tiles < 2) pm = 0;
+    const bool pair = pm > 0;
+    if (pair) prm.total_tiles = 4 * prm.m_pairs * prm.n_blocks;
+    {  // stages: TWO holds only half of the B tile per CTA
+        const int b_cta = (pm == 2 ? prm.n_tile / 2 : prm.n_tile) * 128;
+        const int stage_bytes = (tf32 ? 2 : 1) * (kBlockM * 128 + b_cta);
+        prm.stages = std::min(8, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
+    }
+    cuuint32_t bbox[3] = {(cuuint32_t)kch, (cuuint32_t)(pair ? prm.n_tile / 2 : prm.n_tile), 1};
     int rc = encode_map(&tmA, dt, 4, xs, adims, astr, abox, "A");
     if (!rc) rc = encode_map(&tmB, dt, 3, wg, bdims, bstr, bbox, "B");
     if (!rc && tf32) rc = encode_map(&tmAlo, dt, 4, xs_lo, adims, astr, abox, "A lo");
@@ -554,20 +677,24 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t stage_bytes = (size_t)(tf32 ? 2 : 1) * ((size_t)kBlockM * 128 + (size_t)prm.n_tile * 128);
+    const size_t b_cta = (size_t)(pm == 2 ? prm.n_tile / 2 : prm.n_tile) * 128;
+    const size_t stage_bytes = (size_t)(tf32 ? 2 : 1) * ((size_t)kBlockM * 128 + b_cta);
     const size_t smem = 1024 + prm.stages * stage_bytes + (2 * prm.stages + 4) * 8 + 16;
-    const unsigned grid = (unsigned)std::min<int64_t>(prm.total_tiles, sms);
+    const unsigned grid = pair ? 2 * (unsigned)std::min<int64_t>(prm.total_tiles, sms / 2)
+                               : (unsigned)std::min<int64_t>(prm.total_tiles, sms);
+#define SEGB_K3_LAUNCH(TY_, TF_)                                                                       \
+    rc = pm == 2   ? launch_k3<TY_, TF_, 2>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
+         : pm == 1 ? launch_k3<TY_, TF_, 1>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
+                   : launch_k3<TY_, TF_, 0>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm);
     if (tf32) {
-        cudaFuncSetAttribute(igemm_tconv_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        igemm_tconv_kernel<float, true><<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
+        SEGB_K3_LAUNCH(float, true)
     } else if (s.y_dtype == SEGB_BF16) {
-        cudaFuncSetAttribute(igemm_tconv_kernel<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        igemm_tconv_kernel<__nv_bfloat16, false><<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
+        SEGB_K3_LAUNCH(__nv_bfloat16, false)
     } else {
-        cudaFuncSetAttribute(igemm_tconv_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        igemm_tconv_kernel<float, false><<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
+        SEGB_K3_LAUNCH(float, false)
     }
+#undef SEGB_K3_LAUNCH
+    if (rc) { cudaFreeAsync(xs, st); return rc; }
     note_launch();
     rc = check_launch("igemm_tconv_kernel");
     cudaFreeAsync(xs, st);

@@ -191,3 +191,28 @@ def test_scatter_matches_output_stationary_path(monkeypatch):
     monkeypatch.setenv("SEGB200_IGEMM_NOSCATTER", "1")
     yk = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
     assert O.compare(ys, yk.astype(np.float64), 1e-4, 1e-5)["passed"]
+
+
+@pytest.mark.parametrize("pm", ["0", "1", "2"])
+@pytest.mark.parametrize("name,h,w,ci,n,co,pad,b,compute", [
+    ("odd_m_tiles", 8, 8, 128, 4, 256, 2, 5, "bf16"),     # 5 x 64 positions: 3 blocks, last pair half empty
+    ("pairs_n128", 8, 8, 128, 4, 128, 2, 5, "bf16"),      # 5 x 64 positions: 3 blocks, odd
+    ("pairs_n256_p1", 8, 8, 64, 2, 256, 1, 4, "bf16"),    # odd P on the paired path
+    ("pairs_tf32", 8, 8, 64, 4, 64, 2, 5, "fp32"),        # 3xTF32 through the pair modes
+])
+def test_k3_cta_pair_modes(monkeypatch, pm, name, h, w, ci, n, co, pad, b, compute):
+    """K3 single-CTA (0), B-multicast pair (1) and 2-SM cta_group::2 pair (2) all match the oracle."""
+    import torch
+    monkeypatch.setenv("SEGB200_K3_PAIR", pm)
+    monkeypatch.setenv("SEGB200_IGEMM_GENERIC", "1")
+    x, bank = _inputs(h, w, ci, n, co, b, 4242 + int(pm))
+    if compute == "fp32":
+        x = x.float()
+    layer = P.prepare_layer(bank, pad, compute=compute)
+    y = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
+    xr = x.float().cpu().numpy().astype(np.float64)
+    br = (O.bf16_round(bank) if compute == "bf16" else bank).astype(np.float64)
+    ref = O.forward_segregated_batch(xr, br, pad)
+    tol = (1e-4, 1e-5) if compute == "bf16" else (1e-5, 1e-6)
+    rep = O.compare(y, ref, *tol)
+    assert rep["passed"], (name, pm, rep)
