@@ -57,6 +57,7 @@ struct RowsParams {
     int total_tiles, tiles_per_cta;
     uint32_t slot_bytes, b_tile_bytes;
     int ring;  // input-row slots in the ring (nr <= ring <= kRingMax)
+    int half_tiles;  // RS = 3: tiles of one half of the batch (CTA r of a pair takes half r)
     const void *x;
     void *y;
     unsigned long long *prof;  // optional role cycle counters (CTA 0), SEGB200_PROFILE=1
@@ -182,7 +183,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // MMA issue of one tile for schedule (NH, SWAP, RSEL): the whole warp walks the compile-time
 // schedule (uniform values), lane `leader` issues each tcgen05.mma (no per-MMA branch). The channel-block loop
 // stays rolled so the unrolled schedule's live state stays small.
-template <int NH, int KBC, int SWAP, int MR, int RSEL>
+// CG = 2: one tcgen05.mma.cta_group::2 for a CTA pair (M = 2 MR); each CTA holds the output-
+// channel half of every B tile, so a class's accumulator is N/2 TMEM columns (lanes 0-63: first
+// channel half, lanes 64-127: second).
+template <int NH, int KBC, int SWAP, int MR, int RSEL, int CG = 1>
 __device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t dB0, uint32_t sq, uint32_t ring,
                                            uint32_t S16, uint32_t B16, int N, uint32_t leader) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
@@ -194,19 +198,36 @@ __device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t d
             const MmaGroup g = SCH.g[gi];
             const uint32_t sl = sq + g.du >= ring ? sq + g.du - ring : sq + g.du;  // slot of window row du
             const uint32_t arow = (sl * KBC + kb) * S16 + g.dc * 8;
-            const uint32_t idesc = idesc_bf16_m(MR, g.nc * N);
+            const uint32_t idesc = idesc_bf16_m(MR * CG, g.nc * N);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                tc_mma_pred(d0 + (g.c0 - CB) * N, dA0 + arow + kk * 2, dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2,
-                            idesc, (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
+                tc_mma_any<CG, false>(d0 + (g.c0 - CB) * (N / CG), dA0 + arow + kk * 2,
+                                      dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2, idesc,
+                                      (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
         }
     }
 }
 
 // TMA loads of the resident weights of schedule (NH, SWAP, RSEL), [kb][tile] order
+// (RS = 3: this CTA's output-channel half of every tile, b_tile_bytes = half a tile, counted on
+// the leader's barrier, which expects both halves)
 template <int NH, int KBC, int SWAP, int RSEL>
-__device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB, uint64_t *bar, const RowsParams &prm) {
+__device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB, uint64_t *bar, const RowsParams &prm,
+                                             int pair_rank = -1) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
+    if (pair_rank >= 0) {
+        const uint32_t lb = mapa_rank(bar, 0);
+        if (pair_rank == 0) mbar_expect_tx(bar, 2 * SCH.ntiles * KBC * prm.b_tile_bytes);
+#pragma unroll
+        for (int k = 0; k < SCH.ntiles; ++k) {
+            const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
+            const int tap = prm.cls[c].tap0 + u * NH + v;
+            for (int kb = 0; kb < KBC; ++kb)
+                tma_load_3d_2sm(sB + (kb * SCH.ntiles + k) * prm.b_tile_bytes, tmB, lb, kb * 64,
+                                pair_rank * (prm.c_out / 2), tap);
+        }
+        return;
+    }
     mbar_expect_tx(bar, SCH.ntiles * KBC * prm.b_tile_bytes);
 #pragma unroll
     for (int k = 0; k < SCH.ntiles; ++k) {
@@ -222,9 +243,16 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
 // over a CTA pair by row parity (CTA blockIdx % 2 owns classes (r, 0) and (r, 1)): each CTA
 // then holds half the weights, writes one of the two output rows of a tile and issues 6
 // instead of 11 MMAs per k-step (GAN n = 4, P = 2).
+// RS = 3: a CTA pair (2-CTA cluster) runs one tcgen05.mma.cta_group::2 of M = 2 MR per window
+// group: CTA r streams the rows of batch half r into its own ring (identical slot sequence in
+// both, so one descriptor addresses both) and holds output-channel half r of every weight tile;
+// the leader (rank 0) issues the MMAs; each CTA's TMEM gets its own MR positions with the first
+// channel half in lanes 0-63 and the second in lanes 64-127 (MR = 64), so all four epilogue
+// warps store full 32-lane rows.
 template <int NH, int KBC, int SWAP, int MR, int RS>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const RowsParams prm) {
+    constexpr bool TWO = RS == 3;
     constexpr int NCL = RS == 2 ? 2 : 4;  // parity classes per CTA
     // M = 64 rows with two channel blocks: loader warps 0-1 fill block 0, warps 2-3 block 1 of
     // the same input row at once (else each unit is one (row, block) filled by all four)
@@ -233,7 +261,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int rsel = RS == 2 ? (int)(blockIdx.x % 2) : -1;
-    const int cta = blockIdx.x / RS;
+    const int cta = blockIdx.x / (RS == 1 ? 1 : 2);
+    const int rank = TWO ? (int)cluster_ctarank() : 0;
+    const int toff = TWO ? rank * prm.half_tiles : 0;  // tile index offset of this CTA's batch half
     const int ntiles_b = NCL * NH * NH;
     const RowsSmem L = rows_layout(prm, ntiles_b, KBC);
     uint8_t *sB = smem + L.b;
@@ -248,6 +278,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int N = prm.c_out;
+    constexpr int CG = TWO ? 2 : 1;
     // this CTA's input-row window per class-grid row
     const int dminr = RS == 2 ? prm.dminr_rs[rsel] : prm.dmin_r;
     const int nr = RS == 2 ? NH : prm.nr;
@@ -255,33 +286,43 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(b_full, 1);
         for (int i = 0; i < ring * KBC; ++i) {
-            mbar_init(&slot_full[i], PAIRKB ? 2 : 4);  // one arrival per loader warp filling the slot
+            mbar_init(&slot_full[i], (PAIRKB ? 2 : 4) * CG);  // one arrival per loader warp filling the slot
             mbar_init(&slot_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+            mbar_init(&tempty[i], 4 * CG);  // one arrival per epilogue warp (TWO: of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     }
-    const uint32_t tcols = tmem_pow2(2 * NCL * N);  // 2 buffers x NCL classes x N fp32 columns
+    const uint32_t tcols = tmem_pow2(2 * NCL * N / CG);  // 2 buffers x NCL classes x N (TWO: N/2) columns
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(tcols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (TWO) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (TWO) cluster_sync_all();  // both CTAs' barriers initialised before remote arrivals
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int t0 = cta * prm.tiles_per_cta;
-    const int t1 = min(prm.total_tiles, t0 + prm.tiles_per_cta);
+    const int t1 = min(TWO ? prm.half_tiles : prm.total_tiles, t0 + prm.tiles_per_cta);
     auto loads_of = [&](int t) { return (t == t0 || (t % prm.rows) == 0) ? nr : 1; };
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- the resident weights, in schedule order
-            if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
+            if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank);
+            else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
             else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
             else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
         }
@@ -302,6 +343,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const __nv_bfloat16 *x = reinterpret_cast<const __nv_bfloat16 *>(prm.x);
         const int64_t plane_in = (int64_t)prm.h * prm.w;
         auto load_unit = [&](int t, int l, int kb, uint4 (&r)[8], uint4 &hv) {
+            t += toff;
             const int i = t % prm.rows, rest = t / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
             const int row = i + dminr + l;
@@ -386,7 +428,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
             fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
             __syncwarp();
-            if (lane == 0 && !(ABL(64))) mbar_arrive(&slot_full[sidx]);
+            if (lane == 0 && !(ABL(64))) {
+                if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));  // the leader's barrier
+                else mbar_arrive(&slot_full[sidx]);
+            }
             if (PAIRKB || ckb == KBC - 1) ++q;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -397,8 +442,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             hnxt = hnx2;
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        mbar_wait(b_full, 0);
+        // ---------------- MMA issuer (TWO: the leader CTA issues for the pair)
+        if (!(TWO && rank != 0)) {  // (the peer's MMA warp idles)
+        if (TWO) mbar_wait_cluster(b_full, 0);
+        else mbar_wait(b_full, 0);
         const uint64_t dA0 = desc_k_sw128(smem_u32(sRing)), dB0 = desc_k_sw128(smem_u32(sB));
         const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
         const uint32_t leader = elect_one();
@@ -409,24 +456,34 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             qe += loads_of(t);
             const uint32_t qbase = qe - nr;
             ROWS_PROF(2, pt_)
-            if (!(ABL(32))) mbar_wait(&tempty[acc], acc_phase ^ 1);
+            if (!(ABL(32))) {
+                if (TWO) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                else mbar_wait(&tempty[acc], acc_phase ^ 1);
+            }
             ROWS_PROF(0, pt_)
             for (int l = 0; l < nr; ++l) {
                 const uint32_t q = qbase + l;
 #pragma unroll
                 for (int kb = 0; kb < KBC; ++kb)
-                    if (!(ABL(64))) mbar_wait(&slot_full[(q % ring) * KBC + kb], (q / ring) & 1);
+                    if (!(ABL(64))) {
+                        if (TWO) mbar_wait_cluster(&slot_full[(q % ring) * KBC + kb], (q / ring) & 1);
+                        else mbar_wait(&slot_full[(q % ring) * KBC + kb], (q / ring) & 1);
+                    }
             }
             tc_fence_after();
             ROWS_PROF(1, pt_)
-            const uint32_t d0 = tmem_base + acc * NCL * N;
+            const uint32_t d0 = tmem_base + acc * NCL * (N / CG);
             const uint32_t sq = qbase % ring;
             if (ABL(4)) {
-            } else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
+            } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
+            else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             else issue_tile<NH, KBC, SWAP, MR, 1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             if (elect_one()) {
-                if (!(ABL(32))) tc_commit(&tfull[acc]);
+                if (!(ABL(32))) {
+                    if (TWO) tc_commit_2sm_mc(&tfull[acc], 3);
+                    else tc_commit(&tfull[acc]);
+                }
                 // release input rows no later tile of this strip reads
                 const bool cont = (t + 1 < t1) && ((t + 1) % prm.rows != 0);
                 const int nrel = cont ? 1 : nr;
@@ -434,11 +491,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     const uint32_t q = qbase + l;
 #pragma unroll
                     for (int kb = 0; kb < KBC; ++kb)
-                        if (!(ABL(64))) tc_commit(&slot_empty[(q % ring) * KBC + kb]);
+                        if (!(ABL(64))) {
+                            if (TWO) tc_commit_2sm_mc(&slot_empty[(q % ring) * KBC + kb], 3);
+                            else tc_commit(&slot_empty[(q % ring) * KBC + kb]);
+                        }
                 }
             }
             __syncwarp();
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
         }
     } else {
         // ---------------- epilogue (warps 2..5): warp reads TMEM lane quarter warp % 4. The
@@ -448,8 +509,16 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // is written once, and no staging, proxy fence or barrier is needed.
         const int quarter = warp & 3;
         // position of this lane's TMEM row: M=128 -> lane = row; M=64 -> lanes 32q + [0,16)
-        const int m = MR == 128 ? quarter * 32 + lane : quarter * 16 + (lane & 15);
-        const bool lane_active = MR == 128 || lane < 16;
+        // TWO (M = 64 per CTA): lanes 0-63 = positions with the first channel half, 64-127 = the
+        // same positions with the second half
+        const int m = TWO ? (quarter & 1) * 32 + lane : (MR == 128 ? quarter * 32 + lane : quarter * 16 + (lane & 15));
+        const bool lane_active = TWO || MR == 128 || lane < 16;
+        const int NE = N / CG;                       // TMEM columns (= output channels) per class here
+        const int chalf = TWO ? (quarter >> 1) : 0;  // this warp's output-channel half
+        auto release_acc = [&](int a) {
+            if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
+            else mbar_arrive(&tempty[a]);
+        };
         // With even P the classes with row/column parity 0 fill output row 2i and the even
         // columns; with odd P (SWAP) it is the parity-1 classes (engines.py:338-347).
         constexpr int RE = SWAP, SE = SWAP;  // class parities of output row 2i / even columns
@@ -459,15 +528,16 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = t0; t < t1; ++t) {
-            const int i = t % prm.rows, rest = t / prm.rows;
+            const int ta = t + toff;
+            const int i = ta % prm.rows, rest = ta / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
             long long pe_ = clock64();
             if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (warp == 2) { ROWS_PROF(3, pe_) }
-            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * N;
-            char *pc = reinterpret_cast<char *>(prm.y) + (int64_t)b * prm.c_out * plane_b +
-                       (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co 0, row, col 2j)
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
+            char *pc = reinterpret_cast<char *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE) * plane_b +
+                       (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co, row, col 2j)
             // CH channels per TMEM load per class; the next chunk's loads are in flight while
             // this chunk is converted and stored
             constexpr int CH = kEpiChunk;
@@ -475,13 +545,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             if (ABL(8)) {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0 && !(ABL(32))) mbar_arrive(&tempty[acc]);
+                if (lane == 0 && !(ABL(32))) release_acc(acc);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 continue;
             }
 #pragma unroll
-            for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * N, v[c]);
-            for (int co0 = 0; co0 < N; co0 += CH) {
+            for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE, v[c]);
+            for (int co0 = 0; co0 < NE; co0 += CH) {
                 tmem_wait_ld();
                 uint32_t w[NCL][CH];
 #pragma unroll
@@ -490,17 +560,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
                     for (int k = 0; k < CH; ++k) w[c][k] = v[c][k];
                 }
-                if (co0 + CH < N) {
+                if (co0 + CH < NE) {
 #pragma unroll
-                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * N + co0 + CH, v[c]);
+                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + co0 + CH, v[c]);
                 } else {  // last chunk of the tile: release the accumulator buffer
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    if (lane == 0) release_acc(acc);
                 }
 #pragma unroll
                 for (int k = 0; k < CH; ++k) {
-                    if (RS == 1) {  // class index c = 2r + s; each store is the (even, odd) column pair
+                    if (RS != 2) {  // class index c = 2r + s; each store is the (even, odd) column pair
                         const uint32_t row0 = pack_bf16x2(__uint_as_float(w[2 * RE + SE][k]),
                                                           __uint_as_float(w[2 * RE + (1 - SE)][k]));
                         const uint32_t row1 = pack_bf16x2(__uint_as_float(w[2 * (1 - RE) + SE][k]),
@@ -522,10 +592,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (TWO) cluster_sync_all();  // the leader's MMAs write this CTA's TMEM until both are done
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
+        if (TWO) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tcols));
     }
+    if (TWO) cluster_sync_all();  // remote arrivals on this CTA's barriers are all done
 }
 
 // ---------------------------------------------------------------- host side
@@ -572,6 +645,20 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
     for (int r = 0; r < 2; ++r) prm.dminr_rs[r] = prm.cls[2 * r].base_r - p;
+    // 64-wide class grids with an even batch: a 2-SM CTA pair (nsplit = 3, kernel RS = 3) turns
+    // the half-rate M=64 MMAs into full-rate M=128 ones; each CTA holds the output-channel half
+    // of all weights. SEGB200_ROWS_PAIR=0 disables it (A/B experiments).
+    const char *pe = getenv("SEGB200_ROWS_PAIR");
+    if (mr == 64 && s.batch % 2 == 0 && s.c_out % 32 == 0 && !(pe && !atoi(pe))) {
+        prm.b_tile_bytes = s.c_out / 2 * 128;
+        prm.half_tiles = prm.total_tiles / 2;
+        for (prm.ring = kRingMax; prm.ring > std::max(4, prm.nr); --prm.ring)
+            if (rows_layout(prm, 4 * nh * nh, kbc).total + 1024 <= 227 * 1024) break;
+        if (rows_layout(prm, 4 * nh * nh, kbc).total + 1024 <= 227 * 1024) {
+            nsplit = 3;
+            return true;
+        }
+    }
     prm.b_tile_bytes = s.c_out * 128;
     // all four classes per CTA if their weights fit next to the row ring, else split the
     // classes over a CTA pair by row parity (half the weights each)
@@ -589,6 +676,7 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
 
 // the (NH, KBC, SWAP, MR, NS) variants compiled below
 static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit) {
+    if (nsplit == 3) return mr == 64 && nh == 2;
     if (mr == 128 && nsplit == 1) return true;
     if (mr == 128 && nsplit == 2) return nh == 2 && kbc == 2 && swap == 0;
     if (mr == 64 && nh == 2 && swap == 0) return true;
@@ -604,9 +692,25 @@ bool igemm_rows_supported(const IgemmShape &s) {
 
 template <int NH, int KBC, int SWAP, int MR, int NS>
 static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const RowsParams &prm) {
-    cudaFuncSetAttribute(igemm_rows_kernel<NH, KBC, SWAP, MR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    igemm_rows_kernel<NH, KBC, SWAP, MR, NS><<<grid, kRowsThreads, smem, st>>>(tmB, prm);
+    auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (NS != 3) {
+        kern<<<grid, kRowsThreads, smem, st>>>(tmB, prm);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kRowsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, tmB, prm);
 }
 
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
@@ -619,7 +723,7 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     {
         cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
         cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out_pad * s.c_in_pad * 2};
-        cuuint32_t box[3] = {64, (cuuint32_t)s.c_out, 1};
+        cuuint32_t box[3] = {64, (cuuint32_t)(nsplit == 3 ? s.c_out / 2 : s.c_out), 1};
         cuuint32_t es[3] = {1, 1, 1};
         CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -645,10 +749,19 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int strips = (int)std::min<int64_t>(prm.total_tiles, sms / nsplit);  // CTAs per channel slice
-    const int grid = strips * nsplit;
-    prm.tiles_per_cta = (int)ceil_div(prm.total_tiles, strips);
-    const size_t smem = rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024;
+    int grid;
+    size_t smem;
+    if (nsplit == 3) {  // CTA pairs over the two batch halves
+        const int strips = (int)std::min<int64_t>(prm.half_tiles, sms / 2);
+        grid = 2 * strips;
+        prm.tiles_per_cta = (int)ceil_div(prm.half_tiles, strips);
+        smem = rows_layout(prm, 4 * nh * nh, kbc).total + 1024;
+    } else {
+        const int strips = (int)std::min<int64_t>(prm.total_tiles, sms / nsplit);  // CTAs per channel slice
+        grid = strips * nsplit;
+        prm.tiles_per_cta = (int)ceil_div(prm.total_tiles, strips);
+        smem = rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024;
+    }
     int rc = SEGB_OK;
 #define SEGB_ROWS_CASE(NH_, KBC_, SW_, MR_, NS_)                                                  \
     if (nh == NH_ && kbc == KBC_ && swap == SW_ && mr == MR_ && nsplit == NS_)                     \
@@ -662,6 +775,8 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     SEGB_ROWS_CASE(3, 1, 1, 128, 1) SEGB_ROWS_CASE(3, 2, 0, 128, 1) SEGB_ROWS_CASE(3, 2, 1, 128, 1)
     SEGB_ROWS_CASE(2, 2, 0, 128, 2) SEGB_ROWS_CASE(2, 1, 0, 64, 1) SEGB_ROWS_CASE(2, 1, 0, 64, 2)
     SEGB_ROWS_CASE(2, 2, 0, 64, 1) SEGB_ROWS_CASE(2, 2, 0, 64, 2) SEGB_ROWS_CASE(2, 2, 1, 64, 2)
+    SEGB_ROWS_CASE(2, 1, 0, 64, 3) SEGB_ROWS_CASE(2, 2, 0, 64, 3) SEGB_ROWS_CASE(2, 1, 1, 64, 3)
+    SEGB_ROWS_CASE(2, 2, 1, 64, 3)
     { rc = fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: variant not instantiated"); }
 #undef SEGB_ROWS_CASE
     if (rc) return rc;

@@ -127,6 +127,8 @@ ROWS_CASES = [  # K3b row-streaming variant: class grid cols % 128 == 0, c_out <
     ("rows_m64_l6", 64, 64, 128, 4, 64, 2, 2),      # M=64 rows, 2-way output-channel split
     ("rows_m64_kb1", 32, 64, 64, 4, 32, 2, 2),      # M=64 rows, weights resident unsplit
     ("rows_m64_msub2", 8, 128 + 64 - 64, 128, 4, 64, 2, 2),
+    ("rows_m64_pair_b4", 32, 64, 128, 4, 32, 2, 4),  # 2-SM CTA pairs over the batch halves
+    ("rows_m64_odd_batch", 32, 64, 128, 4, 64, 2, 3),  # odd batch: no pairing
 ]
 
 
@@ -216,3 +218,21 @@ def test_k3_cta_pair_modes(monkeypatch, pm, name, h, w, ci, n, co, pad, b, compu
     tol = (1e-4, 1e-5) if compute == "bf16" else (1e-5, 1e-6)
     rep = O.compare(y, ref, *tol)
     assert rep["passed"], (name, pm, rep)
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", [
+    ("l6_like", 64, 64, 128, 4, 64, 2, 4),
+    ("kb1_c32", 32, 64, 64, 4, 32, 2, 6),
+])
+def test_rows_cta_pair_on_off(monkeypatch, pair, name, h, w, ci, n, co, pad, b):
+    """K3b 64-wide rows as a 2-SM CTA pair (cta_group::2, M=128) or single CTAs (M=64)."""
+    import torch
+    monkeypatch.setenv("SEGB200_ROWS_PAIR", pair)
+    x, bank = _inputs(h, w, ci, n, co, b, 900 + int(pair))
+    layer = P.prepare_layer(bank, pad, compute="bf16")
+    yb = layer.forward(x, path="igemm").float().cpu().numpy()
+    ref = O.forward_segregated_batch(x.float().cpu().numpy().astype(np.float64),
+                                     O.bf16_round(bank).astype(np.float64), pad)
+    rep = O.compare(yb, ref, 2 ** -8 + 1e-4, 1e-6 * float(np.abs(ref).max()))
+    assert rep["passed"], (name, pair, rep)
