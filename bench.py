@@ -222,6 +222,26 @@ def run_reference(args, rank):
     return 0
 
 
+def pin_to_gpu_numa_node(local_rank: int):
+    """Bind this rank's host threads to the CPUs nvidia-smi reports as local to its GPU, so the
+    pinned host buffers of the e2e leg are allocated on the GPU's NUMA node (first touch) and
+    PCIe copies do not cross the socket interconnect. Returns the previous affinity (or None)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local_rank)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * i + b for i, wd in enumerate(words) for b in range(64) if (wd >> b) & 1}
+        prev = os.sched_getaffinity(0)
+        cpus &= prev
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return prev
+    except Exception:  # no NVML or no affinity info: leave the binding alone
+        pass
+    return None
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -234,6 +254,7 @@ def run_ours(args, rank, world, local_rank):
     if args.batch:
         batch = args.batch
     torch.cuda.set_device(local_rank)
+    prev_affinity = None if os.environ.get("SEGB200_NO_NUMA_PIN") else pin_to_gpu_numa_node(local_rank)
     dev = torch.device("cuda", local_rank)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     stream = torch.cuda.current_stream()
@@ -390,13 +411,16 @@ def run_ours(args, rank, world, local_rank):
             ems = float(t.item())
         e2e = {"value": step_macs * world / (ems * 1e-3) / 1e9, "unit": "GMAC/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems,
-               "steps": e2e_steps, "api": "PreparedLayer.forward(pinned host tensor, out=pinned host tensor)"}
+               "steps": e2e_steps, "api": "PreparedLayer.forward(pinned host tensor, out=pinned host tensor)",
+               "host_threads_on_gpu_numa_node": bool(prev_affinity)}
         del hx, hy
 
     if rank != 0:
         return 0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
+        if prev_affinity:  # the CPU baseline gets every host core back
+            os.sched_setaffinity(0, prev_affinity)
         cpu = cpu_baseline(layers, dtype, budget_s=args.cpu_budget)
     total_traffic = sum(s["bytes"] for s in state)
     out = {"metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,

@@ -186,7 +186,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // CG = 2: one tcgen05.mma.cta_group::2 for a CTA pair (M = 2 MR); each CTA holds the output-
 // channel half of every B tile, so a class's accumulator is N/2 TMEM columns (lanes 0-63: first
 // channel half, lanes 64-127: second).
-template <int NH, int KBC, int SWAP, int MR, int RSEL, int CG = 1>
+// COSPLIT (with CG = 2, M = 128): the pair's B rows are [first channel halves | second halves],
+// so class c's accumulator is N/2 columns in both lane halves; otherwise (M = 256) B rows are
+// the group's (class, channel) list split in two and every CTA holds all N columns.
+template <int NH, int KBC, int SWAP, int MR, int RSEL, int CG = 1, bool COSPLIT = true>
 __device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t dB0, uint32_t sq, uint32_t ring,
                                            uint32_t S16, uint32_t B16, int N, uint32_t leader) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
@@ -201,7 +204,7 @@ __device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t d
             const uint32_t idesc = idesc_bf16_m(MR * CG, g.nc * N);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                tc_mma_any<CG, false>(d0 + (g.c0 - CB) * (N / CG), dA0 + arow + kk * 2,
+                tc_mma_any<CG, false>(d0 + (g.c0 - CB) * (COSPLIT ? N / CG : N), dA0 + arow + kk * 2,
                                       dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2, idesc,
                                       (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
         }
@@ -213,8 +216,30 @@ __device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t d
 // the leader's barrier, which expects both halves)
 template <int NH, int KBC, int SWAP, int RSEL>
 __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB, uint64_t *bar, const RowsParams &prm,
-                                             int pair_rank = -1) {
+                                             int pair_rank = -1, bool cosplit = true) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
+    if (pair_rank >= 0 && !cosplit) {
+        // M = 256 pairs: CTA r holds rows [r N/2, (r+1) N/2) of each group's (class, channel)
+        // list, as half tiles: whole tiles of classes c0 + r nc/2 .. (nc >= 2) or the channel
+        // half r of the single class (nc = 1); a group's halves start at half tile b0
+        const uint32_t lb = mapa_rank(bar, 0);
+        if (pair_rank == 0) mbar_expect_tx(bar, 2 * SCH.ntiles * KBC * prm.b_tile_bytes);
+#pragma unroll
+        for (int gi = 0; gi < SCH.count; ++gi) {
+            const MmaGroup g = SCH.g[gi];
+#pragma unroll
+            for (int j = 0; j < g.nc; ++j) {
+                const int k = g.b0 + (g.nc >= 2 ? pair_rank * g.nc / 2 + j / 2 : 0);
+                const int co_off = g.nc >= 2 ? (j & 1) * (prm.c_out / 2) : pair_rank * (prm.c_out / 2);
+                const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
+                const int tap = prm.cls[c].tap0 + u * NH + v;
+                for (int kb = 0; kb < KBC; ++kb)
+                    tma_load_3d_2sm(sB + (kb * SCH.ntiles + g.b0 + j) * prm.b_tile_bytes, tmB, lb, kb * 64, co_off,
+                                    tap);
+            }
+        }
+        return;
+    }
     if (pair_rank >= 0) {
         const uint32_t lb = mapa_rank(bar, 0);
         if (pair_rank == 0) mbar_expect_tx(bar, 2 * SCH.ntiles * KBC * prm.b_tile_bytes);
@@ -252,7 +277,8 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
 template <int NH, int KBC, int SWAP, int MR, int RS>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const RowsParams prm) {
-    constexpr bool TWO = RS == 3;
+    constexpr bool TWO = RS == 3 || RS == 4;  // 2-SM pair: M = 128 (RS 3, MR 64) or 256 (RS 4, MR 128)
+    constexpr bool COSPLIT = RS == 3;
     constexpr int NCL = RS == 2 ? 2 : 4;  // parity classes per CTA
     // M = 64 rows with two channel blocks: loader warps 0-1 fill block 0, warps 2-3 block 1 of
     // the same input row at once (else each unit is one (row, block) filled by all four)
@@ -296,7 +322,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     }
-    const uint32_t tcols = tmem_pow2(2 * NCL * N / CG);  // 2 buffers x NCL classes x N (TWO: N/2) columns
+    const uint32_t tcols = tmem_pow2(2 * NCL * N / (COSPLIT ? 2 : 1));  // 2 buffers x NCL classes x N (RS 3: N/2)
     if (warp == 1) {
         if (TWO) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- the resident weights, in schedule order
-            if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank);
+            if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank, COSPLIT);
             else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
             else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
             else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
@@ -472,10 +498,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
             tc_fence_after();
             ROWS_PROF(1, pt_)
-            const uint32_t d0 = tmem_base + acc * NCL * (N / CG);
+            const uint32_t d0 = tmem_base + acc * NCL * (COSPLIT ? N / 2 : N);
             const uint32_t sq = qbase % ring;
             if (ABL(4)) {
-            } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
+            } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
             else issue_tile<NH, KBC, SWAP, MR, 1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
@@ -511,10 +537,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // position of this lane's TMEM row: M=128 -> lane = row; M=64 -> lanes 32q + [0,16)
         // TWO (M = 64 per CTA): lanes 0-63 = positions with the first channel half, 64-127 = the
         // same positions with the second half
-        const int m = TWO ? (quarter & 1) * 32 + lane : (MR == 128 ? quarter * 32 + lane : quarter * 16 + (lane & 15));
-        const bool lane_active = TWO || MR == 128 || lane < 16;
-        const int NE = N / CG;                       // TMEM columns (= output channels) per class here
-        const int chalf = TWO ? (quarter >> 1) : 0;  // this warp's output-channel half
+        const int m = COSPLIT ? (quarter & 1) * 32 + lane : (MR == 128 ? quarter * 32 + lane : quarter * 16 + (lane & 15));
+        const bool lane_active = COSPLIT || MR == 128 || lane < 16;
+        const int NE = COSPLIT ? N / 2 : N;              // TMEM columns (= output channels) per class here
+        const int chalf = COSPLIT ? (quarter >> 1) : 0;  // this warp's output-channel half
         auto release_acc = [&](int a) {
             if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
             else mbar_arrive(&tempty[a]);
@@ -649,13 +675,18 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     // the half-rate M=64 MMAs into full-rate M=128 ones; each CTA holds the output-channel half
     // of all weights. SEGB200_ROWS_PAIR=0 disables it (A/B experiments).
     const char *pe = getenv("SEGB200_ROWS_PAIR");
-    if (mr == 64 && s.batch % 2 == 0 && s.c_out % 32 == 0 && !(pe && !atoi(pe))) {
+    // 128-wide class grids (nsplit = 4, RS = 4) can likewise pair into M=256 MMAs (half the
+    // weights' shared memory, a deeper row ring, half the B operand reads per SM); measured
+    // slower on ebgan_l7 (0.70 vs 0.64 ms), so only with SEGB200_ROWS_PAIR=4.
+    const bool pair_ok = s.batch % 2 == 0 && s.c_out % 32 == 0 && nh == 2 && !(pe && !atoi(pe));
+    const bool pair128 = pe && atoi(pe) == 4;
+    if (pair_ok && (mr == 64 || pair128)) {
         prm.b_tile_bytes = s.c_out / 2 * 128;
         prm.half_tiles = prm.total_tiles / 2;
         for (prm.ring = kRingMax; prm.ring > std::max(4, prm.nr); --prm.ring)
             if (rows_layout(prm, 4 * nh * nh, kbc).total + 1024 <= 227 * 1024) break;
         if (rows_layout(prm, 4 * nh * nh, kbc).total + 1024 <= 227 * 1024) {
-            nsplit = 3;
+            nsplit = mr == 64 ? 3 : 4;
             return true;
         }
     }
@@ -677,6 +708,7 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
 // the (NH, KBC, SWAP, MR, NS) variants compiled below
 static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit) {
     if (nsplit == 3) return mr == 64 && nh == 2;
+    if (nsplit == 4) return mr == 128 && nh == 2;
     if (mr == 128 && nsplit == 1) return true;
     if (mr == 128 && nsplit == 2) return nh == 2 && kbc == 2 && swap == 0;
     if (mr == 64 && nh == 2 && swap == 0) return true;
@@ -694,7 +726,7 @@ template <int NH, int KBC, int SWAP, int MR, int NS>
 static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const RowsParams &prm) {
     auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (NS != 3) {
+    if (NS < 3) {
         kern<<<grid, kRowsThreads, smem, st>>>(tmB, prm);
         return;
     }
@@ -723,7 +755,7 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     {
         cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
         cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out_pad * s.c_in_pad * 2};
-        cuuint32_t box[3] = {64, (cuuint32_t)(nsplit == 3 ? s.c_out / 2 : s.c_out), 1};
+        cuuint32_t box[3] = {64, (cuuint32_t)(nsplit >= 3 ? s.c_out / 2 : s.c_out), 1};
         cuuint32_t es[3] = {1, 1, 1};
         CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -751,7 +783,7 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid;
     size_t smem;
-    if (nsplit == 3) {  // CTA pairs over the two batch halves
+    if (nsplit >= 3) {  // CTA pairs over the two batch halves
         const int strips = (int)std::min<int64_t>(prm.half_tiles, sms / 2);
         grid = 2 * strips;
         prm.tiles_per_cta = (int)ceil_div(prm.half_tiles, strips);
@@ -776,7 +808,8 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     SEGB_ROWS_CASE(2, 2, 0, 128, 2) SEGB_ROWS_CASE(2, 1, 0, 64, 1) SEGB_ROWS_CASE(2, 1, 0, 64, 2)
     SEGB_ROWS_CASE(2, 2, 0, 64, 1) SEGB_ROWS_CASE(2, 2, 0, 64, 2) SEGB_ROWS_CASE(2, 2, 1, 64, 2)
     SEGB_ROWS_CASE(2, 1, 0, 64, 3) SEGB_ROWS_CASE(2, 2, 0, 64, 3) SEGB_ROWS_CASE(2, 1, 1, 64, 3)
-    SEGB_ROWS_CASE(2, 2, 1, 64, 3)
+    SEGB_ROWS_CASE(2, 2, 1, 64, 3) SEGB_ROWS_CASE(2, 1, 0, 128, 4) SEGB_ROWS_CASE(2, 1, 1, 128, 4)
+    SEGB_ROWS_CASE(2, 2, 0, 128, 4) SEGB_ROWS_CASE(2, 2, 1, 128, 4)
     { rc = fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: variant not instantiated"); }
 #undef SEGB_ROWS_CASE
     if (rc) return rc;

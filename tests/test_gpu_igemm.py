@@ -220,13 +220,16 @@ def test_k3_cta_pair_modes(monkeypatch, pm, name, h, w, ci, n, co, pad, b, compu
     assert rep["passed"], (name, pm, rep)
 
 
-@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("pair", ["0", "1", "4"])
 @pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", [
     ("l6_like", 64, 64, 128, 4, 64, 2, 4),
     ("kb1_c32", 32, 64, 64, 4, 32, 2, 6),
+    ("l7_like", 32, 128, 64, 4, 64, 2, 4),         # "4": M=256 pairs (natural weight halves)
+    ("kb2_c32_128", 32, 128, 128, 4, 32, 2, 4),
 ])
 def test_rows_cta_pair_on_off(monkeypatch, pair, name, h, w, ci, n, co, pad, b):
-    """K3b 64-wide rows as a 2-SM CTA pair (cta_group::2, M=128) or single CTAs (M=64)."""
+    """K3b as 2-SM CTA pairs (cta_group::2: M=128 for 64-wide rows, M=256 for 128-wide ones with
+    SEGB200_ROWS_PAIR=4) or single CTAs."""
     import torch
     monkeypatch.setenv("SEGB200_ROWS_PAIR", pair)
     x, bank = _inputs(h, w, ci, n, co, b, 900 + int(pair))
