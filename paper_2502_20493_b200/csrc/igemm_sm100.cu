@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], TWO ? 8 : 4);  // TWO: the leader's counts both CTAs' epilogues
+            // TWO: the leader's counts its 4 epilogue warps + 1 forwarded arrival from the peer
+            mbar_init(&tempty[i], TWO && rank == 0 ? 5 : 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -157,11 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int S_ = S;
-    // an epilogue warp hands a TMEM accumulator buffer back (TWO: to the leader's barrier)
-    auto release_acc = [&](int a) {
-        if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
-        else mbar_arrive(&tempty[a]);
-    };
+    // an epilogue warp hands a TMEM accumulator buffer back on its own CTA's barrier (a
+    // cluster-scope release right after the global stores would stall on them); TWO: the peer's
+    // idle MMA warp forwards its CTA's completions to the leader
+    auto release_acc = [&](int a) { mbar_arrive(&tempty[a]); };
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -271,6 +271,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 commit(&tfull[acc], false);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        } else if (lane == 0) {  // ---------------- TWO, peer: forward "TMEM buffer drained" to the leader
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            const uint32_t lt[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
+            for (int t = t_begin; t < prm.total_tiles; t += t_step) {
+                const ClassGeom &g = prm.cls[t & 3];
+                const int uses = TF32X3 ? (g.R * g.C * prm.k_cblocks + kTf32Chunk - 1) / kTf32Chunk : 1;
+                for (int k = 0; k < uses; ++k) {
+                    mbar_wait(&tempty[acc], acc_phase);
+                    mbar_arrive_cluster(lt[acc]);
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
             }
         }
     } else if (TF32X3) {  // ---------------- epilogue, 3xTF32: sum the TMEM partials in registers
