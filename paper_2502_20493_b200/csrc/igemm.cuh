@@ -22,6 +22,10 @@ int run_prep_scatter(const void *bank, int bank_dtype, int c_in, int c_in_pad, i
                      cudaStream_t st);
 int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *y, cudaStream_t st);
 
+// K3p: class-pair tiles as 2-SM CTA pairs over K3's operands (igemm_cp_sm100.cu)
+bool igemm_cp_supported(const IgemmShape &s);
+int run_igemm_cp_core(const IgemmShape &s, const void *x_nhwc, const void *wg, void *y, cudaStream_t st);
+
 // stream-ordered workspace pool kept reserved across calls (igemm_sm100.cu)
 void keep_pool_reserved();
 

@@ -655,6 +655,11 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
         note_launch();
         if (int rc = check_launch("nchw->nhwc staging")) { cudaFreeAsync(xs, st); return rc; }
     }
+    if (!tf32 && igemm_cp_supported(s)) {  // K3p: both column parities per tile
+        int rc = run_igemm_cp_core(s, xs, wg, y, st);
+        cudaFreeAsync(xs, st);
+        return rc;
+    }
     const int kch = tf32 ? 32 : 64;
     const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     const int cin_pad = tf32 ? s.c_in_pad32 : s.c_in_pad;

@@ -207,6 +207,7 @@ def test_k3_cta_pair_modes(monkeypatch, pm, name, h, w, ci, n, co, pad, b, compu
     import torch
     monkeypatch.setenv("SEGB200_K3_PAIR", pm)
     monkeypatch.setenv("SEGB200_IGEMM_GENERIC", "1")
+    monkeypatch.setenv("SEGB200_K3_CP", "0")  # the per-class K3 kernel, not the class-pair one
     x, bank = _inputs(h, w, ci, n, co, b, 4242 + int(pm))
     if compute == "fp32":
         x = x.float()
@@ -239,3 +240,28 @@ def test_rows_cta_pair_on_off(monkeypatch, pair, name, h, w, ci, n, co, pad, b):
                                      O.bf16_round(bank).astype(np.float64), pad)
     rep = O.compare(yb, ref, 2 ** -8 + 1e-4, 1e-6 * float(np.abs(ref).max()))
     assert rep["passed"], (name, pair, rep)
+
+
+@pytest.mark.parametrize("cp", ["0", "1"])
+@pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", [
+    ("n4_p2", 16, 16, 128, 4, 128, 2, 3),       # shared middle window, odd batch (half-empty last pair)
+    ("n4_p1_swap", 9, 17, 64, 4, 48, 1, 2),      # odd P: both column classes read every window
+    ("n2_p2_noshare", 7, 15, 64, 2, 64, 2, 4),   # n = 2, even P: the two classes share no window
+    ("n6_p2", 9, 9, 128, 6, 32, 2, 4),
+    ("n4_c96", 8, 8, 256, 4, 96, 2, 2),          # c_out 96: one 96-wide channel block
+])
+def test_k3_class_pair_tiles(monkeypatch, cp, name, h, w, ci, n, co, pad, b):
+    """K3p (both column parities per tile, bf16x2 stores) and the per-class K3 agree with the oracle."""
+    import torch
+    monkeypatch.setenv("SEGB200_IGEMM_GENERIC", "1")
+    monkeypatch.setenv("SEGB200_K3_CP", cp)
+    x, bank = _inputs(h, w, ci, n, co, b, 7000 + int(cp))
+    layer = P.prepare_layer(bank, pad, compute="bf16")
+    ref = O.forward_segregated_batch(x.float().cpu().numpy().astype(np.float64),
+                                     O.bf16_round(bank).astype(np.float64), pad)
+    y32 = layer.forward(x, path="igemm", out_dtype=torch.float32).cpu().numpy()
+    rep = O.compare(y32, ref, 1e-4, 1e-5)
+    assert rep["passed"], (name, cp, rep)
+    yb = layer.forward(x, path="igemm").float().cpu().numpy()
+    repb = O.compare(yb, ref, 2 ** -7, 1e-3 * float(np.abs(ref).max()))
+    assert repb["passed"], (name, cp, repb)
