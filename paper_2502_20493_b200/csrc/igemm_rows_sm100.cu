@@ -29,8 +29,8 @@
 //     output rows with coalesced 4-byte stores (128 B per warp instruction),
 //     the next channels' TMEM loads in flight; every output element written once.
 //
-// Warps: 0 weight TMA, 1 MMA issuer (+TMEM owner), 2..5 epilogue (TMEM lane
-// quarters), 6..9 row loaders / transposers.
+// Warps: 0 weight TMA, 1 MMA issuer (+TMEM owner), 2..9 epilogue (TMEM lane
+// quarter warp % 4, channel half (warp - 2) / 4), 10..13 row loaders / transposers.
 #include <cstdlib>
 #include <mutex>
 
@@ -40,7 +40,14 @@
 namespace segb {
 
 static unsigned long long *g_rows_prof_buf = nullptr;
-constexpr int kRowsThreads = 320;  // 10 warps: weights, MMA, 4 epilogue, 4 loaders
+// epilogue warps: 8 = two per TMEM lane quarter, each storing half of the output channels
+// (twice the TMEM loads and stores in flight of 4 warps)
+#ifndef SEGB_ROWS_EPW
+#define SEGB_ROWS_EPW 4
+#endif
+constexpr int kRowsEpw = SEGB_ROWS_EPW;
+constexpr int kLoaderWarp0 = 2 + kRowsEpw;                   // first of the 4 row-loader warps
+constexpr int kRowsThreads = (kLoaderWarp0 + 4) * 32;        // weights, MMA, epilogue, loaders
 constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
 
 struct RowsClass {
@@ -75,12 +82,18 @@ struct RowsParams {
 
 // role counters: [0] MMA wait tempty, [1] MMA wait slots, [2] MMA issue, [3] epi wait tfull,
 // [4] epi TMEM+convert, [5] epi staging+store, [6] loader wait empty, [7] loader work, [8] tiles
+// (compiled in only with -DSEGB_ROWS_PROFILE: its divergent branches cost the MMA warp its
+// uniform-register descriptor arithmetic)
+#ifdef SEGB_ROWS_PROFILE
 #define ROWS_PROF(idx, t0_)                                                                 \
     if (prm.prof && blockIdx.x == 0) {                                                       \
         const long long _n = clock64();                                                      \
         if ((threadIdx.x & 31) == 0) atomicAdd(&prm.prof[idx], (unsigned long long)(_n - t0_)); \
         t0_ = _n;                                                                            \
     }
+#else
+#define ROWS_PROF(idx, t0_)
+#endif
 
 // ---------------------------------------------------------------------------
 // Compile-time MMA schedule for even n = 2*NH: A window (du, dc) of the slot
@@ -190,23 +203,36 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // so class c's accumulator is N/2 columns in both lane halves; otherwise (M = 256) B rows are
 // the group's (class, channel) list split in two and every CTA holds all N columns.
 template <int NH, int KBC, int SWAP, int MR, int RSEL, int CG = 1, bool COSPLIT = true>
-__device__ __forceinline__ void issue_tile(uint32_t d0, uint64_t dA0, uint64_t dB0, uint32_t sq, uint32_t ring,
+__device__ __forceinline__ void issue_tile(uint32_t d0, uint32_t aLo0, uint32_t bLo0, uint32_t sq, uint32_t ring,
                                            uint32_t S16, uint32_t B16, int N, uint32_t leader) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
     constexpr int CB = RSEL < 0 ? 0 : 2 * RSEL;  // first class held in this CTA's TMEM
+    constexpr int DU = RSEL < 0 ? (SWAP ? NH : NH + 1) : NH;
+    // opaque per-tile copies: keeps ptxas from hoisting all 44 loop-invariant B descriptors out
+    // of the tile loop (more than the uniform register file holds; they were spilled to vector
+    // registers and re-broadcast with R2UR for every MMA)
+    asm volatile("mov.b32 %0, %0;" : "+r"(bLo0));
+    asm volatile("mov.b32 %0, %0;" : "+r"(B16));
+    asm volatile("mov.b32 %0, %0;" : "+r"(d0));
+    // low descriptor word of window row du's slot (channel block 0): the only per-tile values
+    uint32_t arow[DU];
+#pragma unroll
+    for (int du = 0; du < DU; ++du) {
+        const uint32_t sl = sq + du >= ring ? sq + du - ring : sq + du;
+        arow[du] = aLo0 + sl * KBC * S16;
+    }
 #pragma unroll 1
     for (int kb = 0; kb < KBC; ++kb) {
 #pragma unroll
         for (int gi = 0; gi < SCH.count; ++gi) {
             const MmaGroup g = SCH.g[gi];
-            const uint32_t sl = sq + g.du >= ring ? sq + g.du - ring : sq + g.du;  // slot of window row du
-            const uint32_t arow = (sl * KBC + kb) * S16 + g.dc * 8;
+            const uint32_t a = arow[g.du] + kb * S16 + g.dc * 8;
+            const uint32_t b = bLo0 + (kb * SCH.ntiles + g.b0) * B16;
             const uint32_t idesc = idesc_bf16_m(MR * CG, g.nc * N);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                tc_mma_any<CG, false>(d0 + (g.c0 - CB) * (COSPLIT ? N / CG : N), dA0 + arow + kk * 2,
-                                      dB0 + (kb * SCH.ntiles + g.b0) * B16 + kk * 2, idesc,
-                                      (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
+                tc_mma_lo<CG>(d0 + (g.c0 - CB) * (COSPLIT ? N / CG : N), a + kk * 2, b + kk * 2, idesc,
+                              (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
         }
     }
 }
@@ -317,7 +343,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4 * CG);  // one arrival per epilogue warp (TWO: of both CTAs)
+            mbar_init(&tempty[i], kRowsEpw * CG);  // one arrival per epilogue warp (TWO: of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -352,13 +378,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
             else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
         }
-    } else if (warp >= 6) {
+    } else if (warp >= kLoaderWarp0) {
         // ---------------- row loaders / transposers: NCHW input row (64 channels x MR columns
         // + halo) -> K-major SWIZZLE_128B slot rows. Thread (cg = t & 7, cc = t >> 3) loads 8
         // channels x 8 columns with 128-bit loads (coalesced along the row), transposes the 8x8
         // bf16 tile in registers and stores 8 slot rows x 16 B; the next unit's loads are in
         // flight while the current one is stored.
-        const int tt = threadIdx.x - 6 * 32;
+        const int tt = threadIdx.x - kLoaderWarp0 * 32;
         const int tw = tt >> 5;
         const int cg = tt & 7;
         const int cc = PAIRKB ? (tt >> 3) & 7 : tt >> 3;  // column chunk of 8
@@ -401,86 +427,106 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
             }
         };
-        // unit cursor (tile, row of its window, channel block); the loads of the next TWO units
-        // are in flight while the current one waits for its slot and is stored
+        // unit cursor (tile, row of its window, channel block)
         auto advance = [&](int &ut, int &ul, int &ukb) {
             if (++ukb == UKB) {
                 ukb = 0;
                 if (++ul == nr && ++ut < t1) ul = nr - loads_of(ut);
             }
         };
-        int pt = t0, pl = t0 < t1 ? nr - loads_of(t0) : 0, pkb = 0;  // current unit
-        uint4 cur[8], hcur, nxt[8], hnxt;
-        if (pt < t1) load_unit(pt, pl, pkb, cur, hcur);
-        int nt = pt, nl = pl, nkb = pkb;  // next unit
-        if (nt < t1) advance(nt, nl, nkb);
-        if (nt < t1) load_unit(nt, nl, nkb, nxt, hnxt);
-        uint32_t q = 0;
-        while (pt < t1) {
-            const int ckb = PAIRKB ? kbt : pkb;
-            pt = nt; pl = nl; pkb = nkb;  // the unit after this one becomes "next"
-            if (nt < t1) advance(nt, nl, nkb);
-            uint4 nx2[8], hnx2;
-            if (nt < t1) load_unit(nt, nl, nkb, nx2, hnx2);
-            const int sidx = (q % ring) * KBC + ckb;
-            long long pl_ = clock64();
-            if (tw == 0) { ROWS_PROF(7, pl_) }
-            if (!(ABL(64))) mbar_wait(&slot_empty[sidx], ((q / ring) & 1) ^ 1);
-            if (tw == 0) { ROWS_PROF(6, pl_) }
-            const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
-            if (col_active && !(ABL(16))) {
+        // three register buffers in rotation, the loop unrolled by three so that no buffer is
+        // ever copied: a unit's loads are issued three units before its slot stores consume them
+        // (a `cur = nxt` rotation of register arrays made every iteration wait for the loads it
+        // had just issued: one full memory latency per unit)
+        uint4 rb[3][8], hb[3];
+        int bkb[3];     // channel block of the unit in each buffer
+        bool bv[3];     // buffer holds a unit
+        int ct = t0, cl = t0 < t1 ? nr - loads_of(t0) : 0, ckb_ = 0;  // next unit to load
 #pragma unroll
-                for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
-                    uint32_t o[4];
+        for (int k = 0; k < 3; ++k) {
+            bv[k] = ct < t1;
+            bkb[k] = ckb_;
+            if (bv[k]) {
+                load_unit(ct, cl, ckb_, rb[k], hb[k]);
+                advance(ct, cl, ckb_);
+            }
+        }
+        uint32_t qs = 0, qph = 0;  // ring slot and phase of the current input row
+        bool more = bv[0];
+        while (more) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const uint32_t a = (&cur[2 * m].x)[w >> 1], bb = (&cur[2 * m + 1].x)[w >> 1];
-                        o[m] = __byte_perm(a, bb, (w & 1) ? 0x7632 : 0x5410);
+            for (int k = 0; k < 3; ++k) {
+                if (!bv[k]) {
+                    more = false;
+                    break;
+                }
+                const int ckb = PAIRKB ? kbt : bkb[k];
+                const int sidx = qs * KBC + ckb;
+                long long pl_ = clock64();
+                if (tw == 0) { ROWS_PROF(7, pl_) }
+                if (!(ABL(64))) mbar_wait(&slot_empty[sidx], qph ^ 1);
+                if (tw == 0) { ROWS_PROF(6, pl_) }
+                const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
+                if (col_active && !(ABL(16))) {
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {  // 8x8 transpose: column cc*8 + w, channels cg*8 .. +7
+                        uint32_t o[4];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const uint32_t a = (&rb[k][2 * m].x)[w >> 1], bb = (&rb[k][2 * m + 1].x)[w >> 1];
+                            o[m] = __byte_perm(a, bb, (w & 1) ? 0x7632 : 0x5410);
+                        }
+                        const int rho = HL + cc * 8 + w;
+                        const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o[0]), "r"(o[1]),
+                                     "r"(o[2]), "r"(o[3])
+                                     : "memory");
                     }
-                    const int rho = HL + cc * 8 + w;
+                }
+                if (th < (HL + HR) * 8) {
+                    const int hc = th >> 3;
+                    const int rho = hc < HL ? hc : HL + MR + (hc - HL);
                     const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o[0]), "r"(o[1]),
-                                 "r"(o[2]), "r"(o[3])
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(hb[k].x), "r"(hb[k].y),
+                                 "r"(hb[k].z), "r"(hb[k].w)
                                  : "memory");
                 }
+                fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+                __syncwarp();
+                if (lane == 0 && !(ABL(64))) {
+                    if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));  // the leader's barrier
+                    else mbar_arrive(&slot_full[sidx]);
+                }
+                if (PAIRKB || ckb == KBC - 1) {
+                    if (++qs == (uint32_t)ring) { qs = 0; qph ^= 1; }
+                }
+                // refill this buffer with the unit three ahead
+                bv[k] = ct < t1;
+                bkb[k] = ckb_;
+                if (bv[k]) {
+                    load_unit(ct, cl, ckb_, rb[k], hb[k]);
+                    advance(ct, cl, ckb_);
+                }
             }
-            if (th < (HL + HR) * 8) {
-                const int hc = th >> 3;
-                const int rho = hc < HL ? hc : HL + MR + (hc - HL);
-                const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(hcur.x), "r"(hcur.y),
-                             "r"(hcur.z), "r"(hcur.w)
-                             : "memory");
-            }
-            fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
-            __syncwarp();
-            if (lane == 0 && !(ABL(64))) {
-                if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));  // the leader's barrier
-                else mbar_arrive(&slot_full[sidx]);
-            }
-            if (PAIRKB || ckb == KBC - 1) ++q;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                cur[c] = nxt[c];
-                nxt[c] = nx2[c];
-            }
-            hcur = hnxt;
-            hnxt = hnx2;
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (TWO: the leader CTA issues for the pair)
         if (!(TWO && rank != 0)) {  // (the peer's MMA warp idles)
         if (TWO) mbar_wait_cluster(b_full, 0);
         else mbar_wait(b_full, 0);
-        const uint64_t dA0 = desc_k_sw128(smem_u32(sRing)), dB0 = desc_k_sw128(smem_u32(sB));
+        const uint32_t aLo0 = desc_lo_sw128(smem_u32(sRing)), bLo0 = desc_lo_sw128(smem_u32(sB));
         const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
         const uint32_t leader = elect_one();
         int acc = 0;
-        uint32_t acc_phase = 0, qe = 0;
+        uint32_t acc_phase = 0;
+        // ring cursor of the first window row of the current tile (slot, phase) and the tile's
+        // row in its strip, all advanced incrementally: no runtime division in this loop, so
+        // ptxas keeps the slot and descriptor arithmetic in uniform registers (a `% ring` here
+        // went through F2I in vector registers and cost an R2UR per MMA operand)
+        uint32_t sq = 0, phq = 0;
+        int ri = t0 % prm.rows;
         long long pt_ = clock64();
         for (int t = t0; t < t1; ++t) {
-            qe += loads_of(t);
-            const uint32_t qbase = qe - nr;
             ROWS_PROF(2, pt_)
             if (!(ABL(32))) {
                 if (TWO) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
@@ -488,47 +534,51 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
             ROWS_PROF(0, pt_)
             for (int l = 0; l < nr; ++l) {
-                const uint32_t q = qbase + l;
+                uint32_t s = sq + l, ph = phq;
+                if (s >= (uint32_t)ring) { s -= ring; ph ^= 1; }
 #pragma unroll
                 for (int kb = 0; kb < KBC; ++kb)
                     if (!(ABL(64))) {
-                        if (TWO) mbar_wait_cluster(&slot_full[(q % ring) * KBC + kb], (q / ring) & 1);
-                        else mbar_wait(&slot_full[(q % ring) * KBC + kb], (q / ring) & 1);
+                        if (TWO) mbar_wait_cluster(&slot_full[s * KBC + kb], ph);
+                        else mbar_wait(&slot_full[s * KBC + kb], ph);
                     }
             }
             tc_fence_after();
             ROWS_PROF(1, pt_)
             const uint32_t d0 = tmem_base + acc * NCL * (COSPLIT ? N / 2 : N);
-            const uint32_t sq = qbase % ring;
             if (ABL(4)) {
-            } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
-            else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
-            else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
-            else issue_tile<NH, KBC, SWAP, MR, 1>(d0, dA0, dB0, sq, ring, S16, B16, N, leader);
-            if (elect_one()) {
-                if (!(ABL(32))) {
-                    if (TWO) tc_commit_2sm_mc(&tfull[acc], 3);
-                    else tc_commit(&tfull[acc]);
-                }
-                // release input rows no later tile of this strip reads
-                const bool cont = (t + 1 < t1) && ((t + 1) % prm.rows != 0);
-                const int nrel = cont ? 1 : nr;
-                for (int l = 0; l < nrel; ++l) {
-                    const uint32_t q = qbase + l;
-#pragma unroll
-                    for (int kb = 0; kb < KBC; ++kb)
-                        if (!(ABL(64))) {
-                            if (TWO) tc_commit_2sm_mc(&slot_empty[(q % ring) * KBC + kb], 3);
-                            else tc_commit(&slot_empty[(q % ring) * KBC + kb]);
-                        }
-                }
+            } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+            else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+            else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+            else issue_tile<NH, KBC, SWAP, MR, 1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+            // commits, branch-free like the MMAs (lane `leader` issues them)
+            if (!(ABL(32))) {
+                if (TWO) tc_commit_2sm_mc_pred(&tfull[acc], 3, leader);
+                else tc_commit_pred(&tfull[acc], leader);
             }
+            // release input rows no later tile of this strip reads, advance the window
+            const int ri_next = ri + 1 == prm.rows ? 0 : ri + 1;
+            const bool cont = (t + 1 < t1) && ri_next != 0;
+            const int nrel = cont ? 1 : nr;
+            for (int l = 0; l < nrel; ++l) {
+                uint32_t s = sq + l;
+                if (s >= (uint32_t)ring) s -= ring;
+#pragma unroll
+                for (int kb = 0; kb < KBC; ++kb)
+                    if (!(ABL(64))) {
+                        if (TWO) tc_commit_2sm_mc_pred(&slot_empty[s * KBC + kb], 3, leader);
+                        else tc_commit_pred(&slot_empty[s * KBC + kb], leader);
+                    }
+            }
+            sq += nrel;
+            if (sq >= (uint32_t)ring) { sq -= ring; phq ^= 1; }
+            ri = ri_next;
             __syncwarp();
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         }
     } else {
-        // ---------------- epilogue (warps 2..5): warp reads TMEM lane quarter warp % 4. The
+        // ---------------- epilogue (warps 2..): warp reads TMEM lane quarter warp % 4. The
         // classes of a position are in registers, so each lane writes the pair of output
         // columns (2j, 2j+1) of each of its output rows as one 4-byte bf16x2 store: a warp
         // store covers 128 (M=64: 64) contiguous bytes of one output row, every output element
@@ -541,6 +591,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const bool lane_active = COSPLIT || MR == 128 || lane < 16;
         const int NE = COSPLIT ? N / 2 : N;              // TMEM columns (= output channels) per class here
         const int chalf = COSPLIT ? (quarter >> 1) : 0;  // this warp's output-channel half
+        // kRowsEpw = 8: the two warps of a lane quarter split the NE channels of each class
+        const int NEW = NE / (kRowsEpw / 4);             // channels per class this warp stores
+        const int cw0 = ((warp - 2) / 4) * NEW;          // its first channel (TMEM column)
         auto release_acc = [&](int a) {
             if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
             else mbar_arrive(&tempty[a]);
@@ -562,7 +615,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             tc_fence_after();
             if (warp == 2) { ROWS_PROF(3, pe_) }
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
-            char *pc = reinterpret_cast<char *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE) * plane_b +
+            char *pc = reinterpret_cast<char *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE + cw0) * plane_b +
                        (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co, row, col 2j)
             // CH channels per TMEM load per class; the next chunk's loads are in flight while
             // this chunk is converted and stored
@@ -576,8 +629,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 continue;
             }
 #pragma unroll
-            for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE, v[c]);
-            for (int co0 = 0; co0 < NE; co0 += CH) {
+            for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + cw0, v[c]);
+            for (int co0 = 0; co0 < NEW; co0 += CH) {
                 tmem_wait_ld();
                 uint32_t w[NCL][CH];
 #pragma unroll
@@ -586,9 +639,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
                     for (int k = 0; k < CH; ++k) w[c][k] = v[c][k];
                 }
-                if (co0 + CH < NE) {
+                if (co0 + CH < NEW) {
 #pragma unroll
-                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + co0 + CH, v[c]);
+                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + cw0 + co0 + CH, v[c]);
                 } else {  // last chunk of the tile: release the accumulator buffer
                     tc_fence_before();
                     __syncwarp();

@@ -164,6 +164,42 @@ __device__ __forceinline__ void tc_mma_any(uint32_t d_tmem, uint64_t adesc, uint
                      "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
                      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(issue));
 }
+// The same MMA from the low descriptor words: K-major SWIZZLE_128B smem descriptors differ only
+// in their start-address field (bits 0-13 of the low word), so the issue loop carries 32-bit
+// low words (no 64-bit carry chains) and the constant high word is an immediate.
+constexpr uint32_t kDescHiSw128 = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ uint32_t desc_lo_sw128(uint32_t saddr) { return ((saddr >> 4) & 0x3FFF) | (1u << 16); }
+template <int CG>
+__device__ __forceinline__ void tc_mma_lo(uint32_t d_tmem, uint32_t alo, uint32_t blo, uint32_t idesc,
+                                          uint32_t accumulate, uint32_t issue) {
+    if constexpr (CG == 1)
+        asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b64 da, db;\n\t"
+                     "mov.b64 da, {%1, %6};\n\tmov.b64 db, {%2, %6};\n\t"
+                     "setp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                     "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
+                     "r"(alo), "r"(blo), "r"(idesc), "r"(accumulate), "r"(issue), "n"(kDescHiSw128));
+    else
+        asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b64 da, db;\n\t"
+                     "mov.b64 da, {%1, %6};\n\tmov.b64 db, {%2, %6};\n\t"
+                     "setp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                     "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
+                     "r"(alo), "r"(blo), "r"(idesc), "r"(accumulate), "r"(issue), "n"(kDescHiSw128));
+}
+// commits executed by the whole warp, issued by the lane(s) with `issue` != 0
+__device__ __forceinline__ void tc_commit_pred(uint64_t *bar, uint32_t issue) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+                 "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                     smem_u32(bar)),
+                 "r"(issue)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm_mc_pred(uint64_t *bar, uint16_t mask, uint32_t issue) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                 "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                 "%1;\n\t}" ::"r"(smem_u32(bar)),
+                 "h"(mask), "r"(issue)
+                 : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
