@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kCpThreads, 1)
     } else if (warp == 1) {
         if (rank == 0) {  // ---------------- MMA issuer (leader), branch-free over the warp
             const uint32_t leader = elect_one();
+            const uint32_t aLo0 = desc_lo_sw128(smem_u32(sA)), bLo0 = desc_lo_sw128(smem_u32(sB));
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             const uint32_t idesc1 = idesc_bf16_m(2 * kBlockM, NB), idesc2 = idesc_bf16_m(2 * kBlockM, 2 * NB);
@@ -170,17 +171,17 @@ __global__ void __launch_bounds__(kCpThreads, 1)
                         for (int kb = 0; kb < prm.k_cblocks; ++kb) {
                             mbar_wait_cluster(&full[stage], phase);
                             tc_fence_after();
-                            const uint32_t a0 = smem_u32(sA + stage * a_bytes), b0 = smem_u32(sB + stage * b_cta);
+                            const uint32_t a0 = aLo0 + stage * (a_bytes >> 4), b0 = bLo0 + stage * (b_cta >> 4);
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)
-                                tc_mma_any<2, false>(dd, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32), idesc,
-                                                     (fresh && kb == 0 && kk == 0) ? 0u : 1u, leader);
-                            if (leader) tc_commit_2sm_mc(&empty[stage], 3);
+                                tc_mma_lo<2>(dd, a0 + kk * 2, b0 + kk * 2, idesc, (fresh && kb == 0 && kk == 0) ? 0u : 1u,
+                                             leader);
+                            tc_commit_2sm_mc_pred(&empty[stage], 3, leader);
                             __syncwarp();
                             if (++stage == S) { stage = 0; phase ^= 1; }
                         }
                     }
-                if (leader) tc_commit_2sm_mc(&tfull[acc], 3);
+                tc_commit_2sm_mc_pred(&tfull[acc], 3, leader);
                 __syncwarp();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
@@ -216,22 +217,33 @@ __global__ void __launch_bounds__(kCpThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 2 * NB;
+            // the next chunk's TMEM loads are in flight while this chunk is stored
+            uint32_t v0[8], v1[8];
+            tmem_ld8(tl + lo * NB, v0);         // column 2j
+            tmem_ld8(tl + (1 - lo) * NB, v1);   // column 2j + 1
             for (int c0 = 0; c0 < NB; c0 += 8) {
-                uint32_t v0[8], v1[8];
-                tmem_ld8(tl + lo * NB + c0, v0);         // column 2j
-                tmem_ld8(tl + (1 - lo) * NB + c0, v1);   // column 2j + 1
                 tmem_wait_ld();
+                reg_fence8(v0);
+                reg_fence8(v1);
+                uint32_t w0[8], w1[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) { w0[k] = v0[k]; w1[k] = v1[k]; }
+                if (c0 + 8 < NB) {
+                    tmem_ld8(tl + lo * NB + c0 + 8, v0);
+                    tmem_ld8(tl + (1 - lo) * NB + c0 + 8, v1);
+                } else {  // last chunk: the buffer is drained
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                }
                 if (valid) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
                         if (c0 + k < co_left)
-                            store_pair_out<TY>(dst + (int64_t)(c0 + k) * plane, __uint_as_float(v0[k]),
-                                               __uint_as_float(v1[k]));
+                            store_pair_out<TY>(dst + (int64_t)(c0 + k) * plane, __uint_as_float(w0[k]),
+                                               __uint_as_float(w1[k]));
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }

@@ -184,9 +184,18 @@ __device__ __forceinline__ int tile_loads(const RowsParams &p, int t, int t0) {
 
 
 // epilogue TMEM chunk: 8 fp32 columns per class per tcgen05.ld (c_out is a multiple of 16)
-constexpr int kEpiChunk = 8;
-__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[kEpiChunk]) { tmem_ld8(taddr, v); }
-__device__ __forceinline__ void reg_fence_chunk(uint32_t (&v)[kEpiChunk]) { reg_fence8(v); }
+#ifndef SEGB_ROWS_EPI_CHUNK
+#define SEGB_ROWS_EPI_CHUNK 8
+#endif
+constexpr int kEpiChunk = SEGB_ROWS_EPI_CHUNK;
+__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&v)[kEpiChunk]) {
+    if constexpr (kEpiChunk == 16) tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+    else tmem_ld8(taddr, *reinterpret_cast<uint32_t(*)[8]>(&v[0]));
+}
+__device__ __forceinline__ void reg_fence_chunk(uint32_t (&v)[kEpiChunk]) {
+#pragma unroll
+    for (int k = 0; k < kEpiChunk; k += 8) reg_fence8(*reinterpret_cast<uint32_t(*)[8]>(&v[k]));
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

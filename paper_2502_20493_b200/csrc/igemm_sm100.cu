@@ -221,16 +221,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // elected lane issues (branch-free MMAs keep the descriptor math in uniform registers).
         if (!(TWO && rank != 0)) {
             const uint32_t leader = elect_one();
+            const uint32_t aLo0 = desc_lo_sw128(smem_u32(sA)), bLo0 = desc_lo_sw128(smem_u32(sB));
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             const uint32_t idesc = TWO ? (TF32X3 ? idesc_tf32(N) : idesc_bf16(N)) + ((uint32_t)(256 - kBlockM) >> 4 << 24)
                                        : (TF32X3 ? idesc_tf32(N) : idesc_bf16(N));
+            // commits predicated on the elected lane like the MMAs: no divergent branch in the
+            // loop, so ptxas keeps the stage / descriptor arithmetic in uniform registers
             auto commit = [&](uint64_t *bar, bool both) {
-                if (leader) {
-                    if (TWO) tc_commit_2sm_mc(bar, 3);
-                    else if (PAIR && both) tc_commit_mc(bar, 3);
-                    else tc_commit(bar);
-                }
+                if (TWO) tc_commit_2sm_mc_pred(bar, 3, leader);
+                else if (PAIR && both) tc_commit_mc_pred(bar, 3, leader);
+                else tc_commit_pred(bar, leader);
                 __syncwarp();
             };
             for (int t = t_begin; t < prm.total_tiles; t += t_step) {
@@ -252,18 +253,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + stage * NOP * a_bytes), b0 = smem_u32(sB + stage * NOP * b_cta);
+                    // low descriptor words (the start address field moves by 2 per 32 B of K)
+                    const uint32_t a0 = aLo0 + stage * (NOP * a_bytes >> 4), b0 = bLo0 + stage * (NOP * b_cta >> 4);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {  // 4 MMAs of 32 B of K (16 bf16 / 8 tf32) per 128-B row
                         if (TF32X3) {
-                            const uint64_t ah = desc_k_sw128(a0 + kk * 32), al = desc_k_sw128(a0 + a_bytes + kk * 32);
-                            const uint64_t bh = desc_k_sw128(b0 + kk * 32), bl = desc_k_sw128(b0 + b_cta + kk * 32);
-                            tc_mma_any<TWO ? 2 : 1, true>(d, ah, bh, idesc, (kc | kk) != 0, leader);
-                            tc_mma_any<TWO ? 2 : 1, true>(d, ah, bl, idesc, 1, leader);
-                            tc_mma_any<TWO ? 2 : 1, true>(d, al, bh, idesc, 1, leader);
+                            const uint32_t ah = a0 + kk * 2, al = a0 + (a_bytes >> 4) + kk * 2;
+                            const uint32_t bh = b0 + kk * 2, bl = b0 + (b_cta >> 4) + kk * 2;
+                            tc_mma_lo<TWO ? 2 : 1, true>(d, ah, bh, idesc, (kc | kk) != 0, leader);
+                            tc_mma_lo<TWO ? 2 : 1, true>(d, ah, bl, idesc, 1, leader);
+                            tc_mma_lo<TWO ? 2 : 1, true>(d, al, bh, idesc, 1, leader);
                         } else {
-                            tc_mma_any<TWO ? 2 : 1, false>(d, desc_k_sw128(a0 + kk * 32), desc_k_sw128(b0 + kk * 32),
-                                                           idesc, (ks | kk) != 0, leader);
+                            tc_mma_lo<TWO ? 2 : 1, false>(d, a0 + kk * 2, b0 + kk * 2, idesc, (ks | kk) != 0, leader);
                         }
                     }
                     commit(&empty[stage], true);

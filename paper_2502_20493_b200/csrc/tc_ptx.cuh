@@ -169,23 +169,29 @@ __device__ __forceinline__ void tc_mma_any(uint32_t d_tmem, uint64_t adesc, uint
 // low words (no 64-bit carry chains) and the constant high word is an immediate.
 constexpr uint32_t kDescHiSw128 = (1024u >> 4) | (1u << 14) | (2u << 29);
 __device__ __forceinline__ uint32_t desc_lo_sw128(uint32_t saddr) { return ((saddr >> 4) & 0x3FFF) | (1u << 16); }
-template <int CG>
+template <int CG, bool TF = false>
 __device__ __forceinline__ void tc_mma_lo(uint32_t d_tmem, uint32_t alo, uint32_t blo, uint32_t idesc,
                                           uint32_t accumulate, uint32_t issue) {
-    if constexpr (CG == 1)
-        asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b64 da, db;\n\t"
-                     "mov.b64 da, {%1, %6};\n\tmov.b64 db, {%2, %6};\n\t"
-                     "setp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-                     "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
-                     "r"(alo), "r"(blo), "r"(idesc), "r"(accumulate), "r"(issue), "n"(kDescHiSw128));
-    else
-        asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b64 da, db;\n\t"
-                     "mov.b64 da, {%1, %6};\n\tmov.b64 db, {%2, %6};\n\t"
-                     "setp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-                     "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
-                     "r"(alo), "r"(blo), "r"(idesc), "r"(accumulate), "r"(issue), "n"(kDescHiSw128));
+#define SEGB_MMA_LO(KIND)                                                                                  \
+    asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b64 da, db;\n\t"                                         \
+                 "mov.b64 da, {%1, %6};\n\tmov.b64 db, {%2, %6};\n\t"                                        \
+                 "setp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"                                        \
+                 "@q tcgen05.mma." KIND " [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),                           \
+                 "r"(alo), "r"(blo), "r"(idesc), "r"(accumulate), "r"(issue), "n"(kDescHiSw128))
+    if constexpr (CG == 1 && !TF) SEGB_MMA_LO("cta_group::1.kind::f16");
+    else if constexpr (CG == 1 && TF) SEGB_MMA_LO("cta_group::1.kind::tf32");
+    else if constexpr (CG == 2 && !TF) SEGB_MMA_LO("cta_group::2.kind::f16");
+    else SEGB_MMA_LO("cta_group::2.kind::tf32");
+#undef SEGB_MMA_LO
 }
 // commits executed by the whole warp, issued by the lane(s) with `issue` != 0
+__device__ __forceinline__ void tc_commit_mc_pred(uint64_t *bar, uint16_t mask, uint32_t issue) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                 "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                 "%1;\n\t}" ::"r"(smem_u32(bar)),
+                 "h"(mask), "r"(issue)
+                 : "memory");
+}
 __device__ __forceinline__ void tc_commit_pred(uint64_t *bar, uint32_t issue) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
                  "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
@@ -294,6 +300,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
+}
+// 16 lanes x 16 fp32 columns (.16x256b.x2), the fast TMEM read shape (measured on B200 ~5x the
+// bytes per cycle of .32x32b): thread t gets v[0..1] = lane t/4, columns 2(t%4) + {0,1};
+// v[2..3] = lane t/4 + 8, same columns; v[4..7] = the same at columns + 8
+// (tools/probes/tmem_layout_probe.cu, tools/probes/tmem_ld_probe.cu)
+__device__ __forceinline__ void tmem_ld16x256b_x2(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
 }
 // 32 lanes x 8 consecutive fp32 columns
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
