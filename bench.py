@@ -183,6 +183,32 @@ def cpu_baseline(layers, dtype, budget_s: float = 20.0):
             "seconds": total_s}
 
 
+def reference_transient(cfg):
+    """Per-sample transient host memory of the reference's two engines (tracemalloc peak over
+    one forward of the oracle port: np.pad + im2col + GEMM per class, engines.py:271-335, and
+    upsample + pad + im2col, engines.py:258-269), the reference side of BASELINE config 4."""
+    import tracemalloc
+
+    from oracle import segconv_oracle as O
+    name, h, w, ci, n, co, pad = cfg
+    in_seed, bank_seed = O.harness_seeds(0, 0)
+    x = O.gen_synthetic(ci, h, w, in_seed)
+    bank = O.gen_kernel_bank(ci, co, n, bank_seed)
+    out = {}
+    # weights are laid out once per weight tensor outside the forward (engines.py:232-244)
+    prep_seg = O.prepare_segregated(bank, np.float32)
+    prep_ref = np.ascontiguousarray(bank.transpose(1, 0, 2, 3).reshape(co, -1))
+    for key, fn, prep in (("reference_seg_transient_bytes", O.forward_segregated, prep_seg),
+                          ("reference_ref_transient_bytes", O.forward_reference, prep_ref)):
+        tracemalloc.start()
+        y = fn(x, bank, pad, prepared=prep)
+        _, peak = tracemalloc.get_traced_memory()
+        tracemalloc.stop()
+        out[key] = int(peak - y.nbytes)  # transient beyond the returned output
+        del y
+    return out
+
+
 def run_reference(args, rank):
     layers, batch, dtype = WORKLOADS[args.workload]
     if rank != 0:
@@ -270,7 +296,7 @@ def run_ours(args, rank, world, local_rank):
         x = device_unit_floats((batch, ci, h, w), in_seed + rank * batch * ci * h * w, dtype=tdt, device=dev)
         macs, nbytes, (oh, ow) = layer_stats(cfg, batch, dtype)
         y = torch.empty((batch, co, oh, ow), dtype=tdt, device=dev)
-        state.append({"name": name, "layer": layer, "x": x, "y": y, "macs": macs, "bytes": nbytes,
+        state.append({"name": name, "cfg": cfg, "layer": layer, "x": x, "y": y, "macs": macs, "bytes": nbytes,
                       "path": layer.select_path(_lib.BF16 if dtype == "bf16" else _lib.F32, batch, h, w),
                       "flops": 2 * macs})
     torch.cuda.synchronize()
@@ -284,6 +310,19 @@ def run_ours(args, rank, world, local_rank):
         for s in state:
             s["layer"].forward(s["x"], out=s["y"])
     torch.cuda.synchronize()
+
+    # device memory beyond inputs, outputs and prepared weights (BASELINE config 4: memory
+    # footprint vs the reference): the forward workspace high-water mark per layer
+    mem_rows = []
+    for s in state:
+        _lib.workspace_high_water(local_rank, reset=True)
+        s["layer"].forward(s["x"], out=s["y"])
+        torch.cuda.synchronize()
+        mem_rows.append({"name": s["name"], "path": s["path"],
+                         "workspace_bytes": _lib.workspace_high_water(local_rank),
+                         "io_bytes": s["x"].numel() * s["x"].element_size() + s["y"].numel() * s["y"].element_size(),
+                         "upsampled_buffer_bytes_avoided": batch * P.memory_savings_bytes(
+                             s["cfg"][1], s["cfg"][2], s["cfg"][6], s["cfg"][3], element_bytes=s["x"].element_size())})
 
     # CUDA graphs instead of a tracing compiler: each layer's forward (the public API call)
     # is captured once and replayed, so the timed loop has no Python on it. Per-layer events
@@ -422,6 +461,9 @@ def run_ours(args, rank, world, local_rank):
         if prev_affinity:  # the CPU baseline gets every host core back
             os.sched_setaffinity(0, prev_affinity)
         cpu = cpu_baseline(layers, dtype, budget_s=args.cpu_budget)
+        if not args.no_memory_reference:
+            for row, cfg in zip(mem_rows, layers):
+                row.update(reference_transient(cfg))
     total_traffic = sum(s["bytes"] for s in state)
     out = {"metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -434,7 +476,12 @@ def run_ours(args, rank, world, local_rank):
                              f"L2 flushed before every step (256 MB write, untimed); {total_traffic / 1e6:.1f} MB "
                              f"algorithmic traffic per step")},
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-           "clocks": clocks, "layers": layer_rows}
+           "clocks": clocks, "layers": layer_rows,
+           "memory": {"note": "workspace = device bytes segb_forward takes beyond x, y and the prepared "
+                              "weights (batch of the workload); reference_*_transient = tracemalloc peak of "
+                              "one sample through the CPU oracle port of the reference engines; "
+                              "upsampled_buffer_bytes_avoided = memory_savings_bytes (analysis.py:60-82) x batch",
+                      "layers": mem_rows}}
     print(json.dumps(out), flush=True)
     return 0
 
@@ -452,6 +499,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of CUDA-graph replays")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-memory-reference", action="store_true",
+                    help="skip the tracemalloc pass over the CPU oracle (reference memory footprint)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -127,6 +127,13 @@ int segb_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, void *s
 /* number of kernels this library has launched since load (evidence counter) */
 int64_t segb_launch_count(void);
 
+/* forward workspace accounting (no reference counterpart: the reference's
+ * transient buffers are numpy temporaries). High-water mark, in bytes, of the
+ * stream-ordered workspace segb_forward took from `device`'s default memory
+ * pool (K3's NHWC operand copy, K3c's tap products; K2 and K3b take none)
+ * since the last reset; reset != 0 restarts the mark at the current use. */
+int segb_workspace_high_water(int device, int reset, int64_t *bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,24 +132,33 @@ def merge(subs: list[np.ndarray], n: int) -> np.ndarray:
 # --------------------------------------------------------------------------
 # engines.py:271-291 -- the vectorised segregated forward (one sample)
 
-def forward_segregated(x: np.ndarray, bank: np.ndarray, pad: int) -> np.ndarray:
+def prepare_segregated(bank: np.ndarray, dt) -> list[np.ndarray]:
+    """engines.py:236-244: per class (r, s) the contiguous (c_out, c_in*R*C) weight matrix
+    (PreparedLayer.__init__, once per weight tensor, outside the forward)."""
+    c_out = bank.shape[1]
+    return [np.ascontiguousarray(bank[:, :, r::2, s::2].transpose(1, 0, 2, 3).reshape(c_out, -1)).astype(dt)
+            for r in (0, 1) for s in (0, 1)]
+
+
+def forward_segregated(x: np.ndarray, bank: np.ndarray, pad: int, prepared=None) -> np.ndarray:
     """engines.py:236-244 (weight layout) + 271-291 (forward) + 309-335 (GEMM units).
 
     x: (c_in, H, W); bank: (c_in, c_out, n, n). Returns (c_out, M_h, M_w) in
     np.result_type(x, bank). Every output element is written exactly once.
+    prepared: prepare_segregated(bank, dt), else built here.
     """
     c_in, h, w = x.shape
     _, c_out, n, _ = bank.shape
     oh, ow = output_dims(h, w, n, pad)
     p, swap = effective_padding(pad)
     dt = np.result_type(x.dtype, bank.dtype)
+    flats = prepared if prepared is not None else prepare_segregated(bank, dt)
     padded = np.pad(x.astype(dt, copy=False), ((0, 0), (p, p), (p, p)))
     out = np.empty((c_out, oh, ow), dtype=dt)
     for r in (0, 1):
         for s in (0, 1):
-            sub = bank[:, :, r::2, s::2]
-            sh, sw = sub.shape[2], sub.shape[3]
-            flat = np.ascontiguousarray(sub.transpose(1, 0, 2, 3).reshape(c_out, -1)).astype(dt)
+            sh, sw = subkernel_dims(n, r, s)
+            flat = flats[2 * r + s]
             r0, rows, rb = parity_grid(oh, r, swap)
             c0, cols, cb = parity_grid(ow, s, swap)
             if rows == 0 or cols == 0:
@@ -175,8 +184,9 @@ def forward_segregated_batch(x: np.ndarray, bank: np.ndarray, pad: int,
 # --------------------------------------------------------------------------
 # engines.py:134-140, 258-269, tensors.py:76-112 -- Alg. 1 (bed of nails)
 
-def forward_reference(x: np.ndarray, bank: np.ndarray, pad: int) -> np.ndarray:
-    """Upsample (zero insertion) -> zero pad P -> valid correlation, unflipped kernel."""
+def forward_reference(x: np.ndarray, bank: np.ndarray, pad: int, prepared=None) -> np.ndarray:
+    """Upsample (zero insertion) -> zero pad P -> valid correlation, unflipped kernel.
+    prepared: the (c_out, c_in*n*n) weight matrix (engines.py:232-235), else built here."""
     c_in, h, w = x.shape
     _, c_out, n, _ = bank.shape
     oh, ow = output_dims(h, w, n, pad)
@@ -185,7 +195,8 @@ def forward_reference(x: np.ndarray, bank: np.ndarray, pad: int) -> np.ndarray:
     up[:, pad:pad + 2 * h - 1:2, pad:pad + 2 * w - 1:2] = x
     win = sliding_window_view(up, (n, n), axis=(1, 2))
     patches = win.transpose(1, 2, 0, 3, 4).reshape(oh * ow, -1)
-    flat = bank.transpose(1, 0, 2, 3).reshape(c_out, -1).astype(dt)
+    flat = prepared if prepared is not None else np.ascontiguousarray(
+        bank.transpose(1, 0, 2, 3).reshape(c_out, -1)).astype(dt)
     return (patches @ flat.T).T.reshape(c_out, oh, ow)
 
 

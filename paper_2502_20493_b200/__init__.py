@@ -24,6 +24,7 @@ from .spec import (
     EffectivePadding,
     TransposeConvSpec,
     effective_padding,
+    memory_savings_bytes,
     mult_count_segregated,
     output_dims,
     subkernel_dims,
@@ -32,7 +33,7 @@ from .spec import (
 __all__ = [
     "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "EffectivePadding",
     "PreparedLayer", "ShapeError", "SpecError", "SubKernelSet", "TransposeConvSpec",
-    "compare_outputs", "effective_padding", "layer_forward", "merge_subkernels",
+    "compare_outputs", "effective_padding", "layer_forward", "memory_savings_bytes", "merge_subkernels",
     "mult_count_segregated", "output_dims", "prepare_layer", "segregate_kernel",
     "subkernel_dims", "transpose_conv_reference", "transpose_conv_segregated",
 ]

@@ -168,6 +168,22 @@ const char *segb_last_error(void) { return g_err.c_str(); }
 
 int64_t segb_launch_count(void) { return g_launches.load(); }
 
+int segb_workspace_high_water(int device, int reset, int64_t *bytes) {
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "default memory pool: %s", cudaGetErrorString(e));
+    if (reset) {
+        unsigned long long zero = 0;
+        e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "memory pool reset: %s", cudaGetErrorString(e));
+    }
+    unsigned long long high = 0;
+    e = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high);
+    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "memory pool query: %s", cudaGetErrorString(e));
+    if (bytes) *bytes = (int64_t)high;
+    return SEGB_OK;
+}
+
 int segb_output_dims(int in_h, int in_w, int kernel_n, int pad, int *out_h, int *out_w) {
     return check_spec(in_h, in_w, kernel_n, pad, 1, 1, out_h, out_w);
 }

@@ -138,8 +138,68 @@ __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
     for (int j = 0; j < WC; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
     const TX *xw = xb + (int64_t)row0 * a.w_in + col0;  // window origin of channel 0 (may point outside)
 
+    auto load_win = [&](TC (&dst)[WR][WC], int ci_abs) {
+        const TX *xc = xw + (int64_t)ci_abs * plane;
+        if (warp_inside) {  // one row pointer per window row, immediate column offsets
+#pragma unroll
+            for (int i = 0; i < WR; ++i) {
+                const TX *rp = xc + i * a.w_in;
+#pragma unroll
+                for (int j = 0; j < WC; ++j) dst[i][j] = load_x<TX, TC, RBF>(rp + j);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < WR; ++i) {
+                const TX *rp = xc + i * a.w_in;
+#pragma unroll
+                for (int j = 0; j < WC; ++j) dst[i][j] = (rok[i] && cok[j]) ? load_x<TX, TC, RBF>(rp + j) : TC(0);
+            }
+        }
+    };
+    auto compute = [&](const TC (&win)[WR][WC], int ci) {
+#pragma unroll
+        for (int c = 0; c < COB; ++c) {
+            const TC *wp = ws + (c * kDirectCiChunk + ci) * N2P;
+            TC wv[N2P];
+            load_taps<TC, N2P>(wp, wv);  // 128-bit shared-memory broadcasts
+#pragma unroll
+            for (int qq = 0; qq < RQ; ++qq)
+#pragma unroll
+                for (int cq = 0; cq < CQ; ++cq) {
+#pragma unroll
+                    for (int u = 0; u < R0; ++u) {
+#pragma unroll
+                        for (int v = 0; v < R0; ++v)
+                            acc[c][2 * qq][2 * cq] += win[qq + u][cq + v] * wv[u * R0 + v];
+#pragma unroll
+                        for (int v = 0; v < R1; ++v)
+                            acc[c][2 * qq][2 * cq + 1] += win[qq + u][cq + 1 + v] * wv[OFF1 + u * R1 + v];
+                    }
+#pragma unroll
+                    for (int u = 0; u < R1; ++u) {
+#pragma unroll
+                        for (int v = 0; v < R0; ++v)
+                            acc[c][2 * qq + 1][2 * cq] += win[qq + 1 + u][cq + v] * wv[OFF2 + u * R0 + v];
+#pragma unroll
+                        for (int v = 0; v < R1; ++v)
+                            acc[c][2 * qq + 1][2 * cq + 1] += win[qq + 1 + u][cq + 1 + v] * wv[OFF3 + u * R1 + v];
+                    }
+                }
+        }
+    };
+
+    // Software pipeline over input channels with two window buffers used alternately (no
+    // register copies): the next channel's window loads are in flight while the current one
+    // is multiplied, and the first window of a weight chunk is loaded before the chunk's
+    // weights are staged.
+    // Pipelined only with three or more output channels per thread (enough arithmetic per
+    // window to cover a load); with fewer the second window's registers cost more occupancy
+    // than the overlap gains (measured on the dataset layers).
+    constexpr bool PIPE = COB >= 3;
+    TC wa[WR][WC], wb[WR][WC];
     for (int ci0 = 0; ci0 < a.c_in; ci0 += kDirectCiChunk) {
         const int nci = min(kDirectCiChunk, a.c_in - ci0);
+        if (PIPE) load_win(wa, ci0);
         __syncthreads();
         for (int i = tid; i < COB * nci * N2P; i += 32 * kDirectRowsPerBlock) {
             const int co = i / (nci * N2P);
@@ -150,54 +210,19 @@ __global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
                 (co0 + co < a.c_out) ? wsrc[((int64_t)(co0 + co) * a.c_in + ci0 + ci) * N2P + k] : TC(0);
         }
         __syncthreads();
-#pragma unroll 2
-        for (int ci = 0; ci < nci; ++ci) {
-            const TX *xc = xw + (int64_t)(ci0 + ci) * plane;
-            TC win[WR][WC];
-            if (warp_inside) {  // one row pointer per window row, immediate column offsets
-#pragma unroll
-                for (int i = 0; i < WR; ++i) {
-                    const TX *rp = xc + i * a.w_in;
-#pragma unroll
-                    for (int j = 0; j < WC; ++j) win[i][j] = load_x<TX, TC, RBF>(rp + j);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < WR; ++i) {
-                    const TX *rp = xc + i * a.w_in;
-#pragma unroll
-                    for (int j = 0; j < WC; ++j) win[i][j] = (rok[i] && cok[j]) ? load_x<TX, TC, RBF>(rp + j) : TC(0);
-                }
+        if constexpr (PIPE) {
+            for (int ci = 0; ci < nci; ci += 2) {
+                if (ci + 1 < nci) load_win(wb, ci0 + ci + 1);
+                compute(wa, ci);
+                if (ci + 1 >= nci) break;
+                if (ci + 2 < nci) load_win(wa, ci0 + ci + 2);
+                compute(wb, ci + 1);
             }
-#pragma unroll
-            for (int c = 0; c < COB; ++c) {
-                const TC *wp = ws + (c * kDirectCiChunk + ci) * N2P;
-                TC wv[N2P];
-                load_taps<TC, N2P>(wp, wv);  // 128-bit shared-memory broadcasts
-#pragma unroll
-                for (int qq = 0; qq < RQ; ++qq)
-#pragma unroll
-                    for (int cq = 0; cq < CQ; ++cq) {
-#pragma unroll
-                        for (int u = 0; u < R0; ++u) {
-#pragma unroll
-                            for (int v = 0; v < R0; ++v)
-                                acc[c][2 * qq][2 * cq] += win[qq + u][cq + v] * wv[u * R0 + v];
-#pragma unroll
-                            for (int v = 0; v < R1; ++v)
-                                acc[c][2 * qq][2 * cq + 1] += win[qq + u][cq + 1 + v] * wv[OFF1 + u * R1 + v];
-                        }
-#pragma unroll
-                        for (int u = 0; u < R1; ++u) {
-#pragma unroll
-                            for (int v = 0; v < R0; ++v)
-                                acc[c][2 * qq + 1][2 * cq] += win[qq + 1 + u][cq + v] * wv[OFF2 + u * R0 + v];
-#pragma unroll
-                            for (int v = 0; v < R1; ++v)
-                                acc[c][2 * qq + 1][2 * cq + 1] +=
-                                    win[qq + 1 + u][cq + 1 + v] * wv[OFF3 + u * R1 + v];
-                        }
-                    }
+        } else {
+#pragma unroll 2
+            for (int ci = 0; ci < nci; ++ci) {
+                load_win(wa, ci0 + ci);
+                compute(wa, ci);
             }
         }
     }

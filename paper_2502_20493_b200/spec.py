@@ -90,3 +90,28 @@ def algorithmic_bytes(spec: TransposeConvSpec, batch: int, x_bytes: int, y_bytes
     return (batch * spec.c_in * spec.in_h * spec.in_w * x_bytes
             + batch * spec.c_out * oh * ow * y_bytes
             + spec.c_in * spec.c_out * spec.kernel_n ** 2 * w_bytes)
+
+
+SAVINGS_UPSAMPLED_TOTAL = "upsampled_total"
+SAVINGS_UPSAMPLED_MINUS_INPUT = "upsampled_minus_input"
+
+
+def memory_savings_bytes(in_h: int, in_w: int, pad: int, c_in: int,
+                         mode: str = SAVINGS_UPSAMPLED_TOTAL, element_bytes: int = 4) -> int:
+    """analysis.py:60-82: bytes of the bed-of-nails upsampled (and padded) buffer the segregated
+    engine never allocates, per sample -- the paper's memory-savings figure. mode
+    "upsampled_minus_input" nets out the floor(P/2)-padded raw input buffer."""
+    if in_h < 1 or in_w < 1 or c_in < 1:
+        raise SpecError(f"dims must be >= 1, got {in_h}x{in_w} with {c_in} channels")
+    if pad < 0:
+        raise SpecError(f"padding must be >= 0, got {pad}")
+    if element_bytes < 1:
+        raise SpecError(f"element size must be >= 1 byte, got {element_bytes}")
+    upsampled = (2 * in_h - 1 + 2 * pad) * (2 * in_w - 1 + 2 * pad) * c_in * element_bytes
+    if mode == SAVINGS_UPSAMPLED_TOTAL:
+        return upsampled
+    if mode == SAVINGS_UPSAMPLED_MINUS_INPUT:
+        eff = pad // 2
+        return upsampled - (in_h + 2 * eff) * (in_w + 2 * eff) * c_in * element_bytes
+    raise ValueError(f"unknown savings mode {mode!r}, expected one of "
+                     f"{(SAVINGS_UPSAMPLED_TOTAL, SAVINGS_UPSAMPLED_MINUS_INPUT)}")

@@ -123,3 +123,23 @@ def test_c_abi_error_codes():
     h = ctypes.c_void_p()
     assert lib.segb_prepare(None, 0, 1, 1, 3, 0, 7, 0, None, ctypes.byref(h)) == _lib.SEGB_ERR_VALUE
     assert lib.segb_forward(None, None, 0, 1, 4, 4, None, 0, 0, 0, None) == _lib.SEGB_ERR_VALUE
+
+
+# analysis.py:60-82 memory_savings_bytes, pinned to the reference's own figures
+# (/root/reference/pkg/tests/test_analysis.py:99-125: the paper's Table 4 bytes, pad 2, fp32)
+@pytest.mark.parametrize("side,channels,expected", [
+    (4, 1024, 495_616), (8, 512, 739_328), (16, 256, 1_254_400), (32, 128, 2_298_368),
+    (4, 512, 247_808), (8, 256, 369_664), (4, 2048, 991_232), (8, 1024, 1_478_656),
+    (16, 512, 2_508_800), (32, 256, 4_596_736), (64, 128, 8_786_432), (128, 64, 17_172_736)])
+def test_memory_savings_gan_layers(side, channels, expected):
+    assert P.memory_savings_bytes(side, side, 2, channels) == expected
+
+
+def test_memory_savings_image_pipeline_and_errors():
+    assert P.memory_savings_bytes(224, 224, 2, 3, "upsampled_minus_input") == 1_827_900
+    with pytest.raises(P.SpecError):
+        P.memory_savings_bytes(0, 4, 2, 3)
+    with pytest.raises(P.SpecError):
+        P.memory_savings_bytes(4, 4, -1, 3)
+    with pytest.raises(ValueError):
+        P.memory_savings_bytes(4, 4, 2, 3, "nope")
