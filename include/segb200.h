@@ -120,6 +120,21 @@ int segb_select_path(const segb_layer *layer, int x_dtype, int64_t batch, int in
 
 int segb_release(segb_layer *layer);
 
+/* Layer stacks (the reference's GAN_SUITE generator stacks,
+ * bench.py:124-139, which a reference user runs as one layer_forward per layer,
+ * engines.py:163-172, through host arrays). layers[0..count) are chained: layer
+ * i's output (batch, c_out_i, h_i, w_i) is layer i+1's input, so c_out_i must
+ * equal c_in_{i+1} (SEGB_ERR_SHAPE otherwise). Intermediates live in the
+ * caller's device workspace in inter_dtype (two ping-pong buffers; the size is
+ * segb_stack_workspace_bytes); each layer runs with its own compute dtype and
+ * the kernel segb_forward's SEGB_PATH_AUTO picks. Nothing is copied to the
+ * host between layers; all launches go to `stream` (capturable as one graph). */
+int segb_stack_workspace_bytes(const segb_layer *const *layers, int count, int64_t batch, int in_h,
+                               int in_w, int inter_dtype, int64_t *bytes);
+int segb_stack_forward(const segb_layer *const *layers, int count, const void *x, int x_dtype,
+                       int64_t batch, int in_h, int in_w, void *y, int y_dtype, int inter_dtype,
+                       void *workspace, int64_t workspace_bytes, void *stream);
+
 /* synth.py:28-39 unit_floats on device: out[i] = float32(float64(
  * splitmix64(seed + i)) * 2^-64), optionally rounded on to bf16. */
 int segb_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, void *stream);

@@ -20,6 +20,7 @@ from .engines import (
 )
 from .errors import ShapeError, SpecError
 from .segregation import SubKernelSet, merge_subkernels, segregate_kernel
+from .stack import PreparedStack, prepare_stack
 from .spec import (
     EffectivePadding,
     TransposeConvSpec,
@@ -32,8 +33,8 @@ from .spec import (
 
 __all__ = [
     "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "EffectivePadding",
-    "PreparedLayer", "ShapeError", "SpecError", "SubKernelSet", "TransposeConvSpec",
+    "PreparedLayer", "PreparedStack", "ShapeError", "SpecError", "SubKernelSet", "TransposeConvSpec",
     "compare_outputs", "effective_padding", "layer_forward", "memory_savings_bytes", "merge_subkernels",
-    "mult_count_segregated", "output_dims", "prepare_layer", "segregate_kernel",
+    "mult_count_segregated", "output_dims", "prepare_layer", "prepare_stack", "segregate_kernel",
     "subkernel_dims", "transpose_conv_reference", "transpose_conv_segregated",
 ]

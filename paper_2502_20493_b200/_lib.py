@@ -39,6 +39,8 @@ SIGNATURES = {
     "segb_release": (_i, [_p]),
     "segb_unit_floats": (_i, [_p, _i, _i64, _u64, _p]),
     "segb_workspace_high_water": (_i, [_i, _i, ctypes.POINTER(_i64)]),
+    "segb_stack_workspace_bytes": (_i, [ctypes.POINTER(_p), _i, _i64, _i, _i, _i, ctypes.POINTER(_i64)]),
+    "segb_stack_forward": (_i, [ctypes.POINTER(_p), _i, _p, _i, _i64, _i, _i, _p, _i, _i, _p, _i64, _p]),
 }
 
 _lib = None

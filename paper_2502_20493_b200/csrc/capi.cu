@@ -350,6 +350,72 @@ int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch
     }
 }
 
+// ---------------------------------------------------------------- layer stacks
+// the GAN_SUITE generator stacks (bench.py:124-139 of the reference) run
+// device-resident. The reference has no stack call: a user chains layer_forward (engines.py:
+// 163-172) per layer through host arrays. Here layer i's output is layer i+1's input in the
+// caller's workspace (two ping-pong buffers of the largest intermediate, inter_dtype), so
+// nothing crosses PCIe between layers and the whole chain is one stream-ordered launch
+// sequence (capturable as one CUDA graph).
+
+static int stack_plan(const segb_layer *const *layers, int count, int64_t batch, int in_h, int in_w,
+                      int inter_dtype, int64_t *inter_elems) {
+    if (!layers || count < 1) return fail(SEGB_ERR_VALUE, "a stack needs at least one layer");
+    if (batch < 1) return fail(SEGB_ERR_SHAPE, "batch must be >= 1, got %lld", (long long)batch);
+    if (!valid_dtype(inter_dtype)) return fail(SEGB_ERR_VALUE, "unknown intermediate dtype %d", inter_dtype);
+    int h = in_h, w = in_w;
+    int64_t most = 0;
+    for (int i = 0; i < count; ++i) {
+        const segb_layer *L = layers[i];
+        if (!L) return fail(SEGB_ERR_VALUE, "null layer %d in the stack", i);
+        if (i > 0 && layers[i - 1]->c_out != L->c_in)
+            return fail(SEGB_ERR_SHAPE, "stack layer %d expects %d input channels, layer %d produces %d", i, L->c_in,
+                        i - 1, layers[i - 1]->c_out);
+        int oh, ow;
+        if (int rc = check_spec(h, w, L->n, L->pad, L->c_in, L->c_out, &oh, &ow)) return rc;
+        if (i + 1 < count) most = std::max<int64_t>(most, batch * L->c_out * (int64_t)oh * ow);
+        h = oh;
+        w = ow;
+    }
+    if (inter_elems) *inter_elems = most;
+    return SEGB_OK;
+}
+
+int segb_stack_workspace_bytes(const segb_layer *const *layers, int count, int64_t batch, int in_h, int in_w,
+                               int inter_dtype, int64_t *bytes) {
+    int64_t most = 0;
+    if (int rc = stack_plan(layers, count, batch, in_h, in_w, inter_dtype, &most)) return rc;
+    const int64_t one = (most * (int64_t)dtype_size(inter_dtype) + 255) / 256 * 256;
+    if (bytes) *bytes = count > 2 ? 2 * one : one;
+    return SEGB_OK;
+}
+
+int segb_stack_forward(const segb_layer *const *layers, int count, const void *x, int x_dtype, int64_t batch,
+                       int in_h, int in_w, void *y, int y_dtype, int inter_dtype, void *workspace,
+                       int64_t workspace_bytes, void *stream) {
+    int64_t need = 0;
+    if (int rc = segb_stack_workspace_bytes(layers, count, batch, in_h, in_w, inter_dtype, &need)) return rc;
+    if (!x || !y) return fail(SEGB_ERR_VALUE, "null tensor");
+    if (need > 0 && (!workspace || workspace_bytes < need))
+        return fail(SEGB_ERR_VALUE, "stack workspace of %lld bytes needed, got %lld", (long long)need,
+                    (long long)workspace_bytes);
+    const int64_t half = count > 2 ? need / 2 : need;
+    const void *cur = x;
+    int cur_dt = x_dtype, h = in_h, w = in_w;
+    for (int i = 0; i < count; ++i) {
+        const bool last = i + 1 == count;
+        void *dst = last ? y : (char *)workspace + (i % 2) * half;
+        const int dst_dt = last ? y_dtype : inter_dtype;
+        if (int rc = segb_forward(layers[i], cur, cur_dt, batch, h, w, dst, dst_dt, -1, SEGB_PATH_AUTO, stream))
+            return rc;
+        h = 2 * h + 2 * layers[i]->pad - layers[i]->n;
+        w = 2 * w + 2 * layers[i]->pad - layers[i]->n;
+        cur = dst;
+        cur_dt = dst_dt;
+    }
+    return SEGB_OK;
+}
+
 int segb_release(segb_layer *L) {
     if (!L) return SEGB_OK;
     cudaFree(L->bank);

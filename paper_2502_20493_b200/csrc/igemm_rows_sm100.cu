@@ -639,18 +639,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
 #pragma unroll
             for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + cw0, v[c]);
-            for (int co0 = 0; co0 < NEW; co0 += CH) {
+            // two register buffers used alternately (loop unrolled by two, no copies): after
+            // the wait for chunk k's loads, chunk k+1's loads go into the other buffer while
+            // chunk k is converted and stored
+            uint32_t v2[NCL][CH];
+            auto chunk = [&](int co0, uint32_t (&cur)[NCL][CH], uint32_t (&nxt)[NCL][CH]) {
                 tmem_wait_ld();
-                uint32_t w[NCL][CH];
 #pragma unroll
-                for (int c = 0; c < NCL; ++c) {
-                    reg_fence_chunk(v[c]);
-#pragma unroll
-                    for (int k = 0; k < CH; ++k) w[c][k] = v[c][k];
-                }
+                for (int c = 0; c < NCL; ++c) reg_fence_chunk(cur[c]);
                 if (co0 + CH < NEW) {
 #pragma unroll
-                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + cw0 + co0 + CH, v[c]);
+                    for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + cw0 + co0 + CH, nxt[c]);
                 } else {  // last chunk of the tile: release the accumulator buffer
                     tc_fence_before();
                     __syncwarp();
@@ -659,20 +658,24 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
                 for (int k = 0; k < CH; ++k) {
                     if (RS != 2) {  // class index c = 2r + s; each store is the (even, odd) column pair
-                        const uint32_t row0 = pack_bf16x2(__uint_as_float(w[2 * RE + SE][k]),
-                                                          __uint_as_float(w[2 * RE + (1 - SE)][k]));
-                        const uint32_t row1 = pack_bf16x2(__uint_as_float(w[2 * (1 - RE) + SE][k]),
-                                                          __uint_as_float(w[2 * (1 - RE) + (1 - SE)][k]));
+                        const uint32_t row0 = pack_bf16x2(__uint_as_float(cur[2 * RE + SE][k]),
+                                                          __uint_as_float(cur[2 * RE + (1 - SE)][k]));
+                        const uint32_t row1 = pack_bf16x2(__uint_as_float(cur[2 * (1 - RE) + SE][k]),
+                                                          __uint_as_float(cur[2 * (1 - RE) + (1 - SE)][k]));
                         if (lane_active && !(ABL(1))) {
                             *reinterpret_cast<uint32_t *>(pc) = row0;
                             *reinterpret_cast<uint32_t *>(pc + ow_b) = row1;
                         }
                     } else {  // TMEM slot = column parity s
-                        const uint32_t row = pack_bf16x2(__uint_as_float(w[SE][k]), __uint_as_float(w[1 - SE][k]));
+                        const uint32_t row = pack_bf16x2(__uint_as_float(cur[SE][k]), __uint_as_float(cur[1 - SE][k]));
                         if (lane_active && !(ABL(1))) *reinterpret_cast<uint32_t *>(pc) = row;
                     }
                     pc += plane_b;
                 }
+            };
+            for (int co0 = 0; co0 < NEW; co0 += 2 * CH) {
+                chunk(co0, v, v2);
+                if (co0 + CH < NEW) chunk(co0 + CH, v2, v);
             }
             if (warp == 2) { ROWS_PROF(4, pe_) }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }

@@ -143,3 +143,14 @@ def test_memory_savings_image_pipeline_and_errors():
         P.memory_savings_bytes(4, 4, -1, 3)
     with pytest.raises(ValueError):
         P.memory_savings_bytes(4, 4, 2, 3, "nope")
+
+
+def test_stack_c_abi_validation():
+    lib = _lib.lib()
+    v = ctypes.c_int64()
+    assert lib.segb_stack_workspace_bytes(None, 0, 1, 4, 4, _lib.BF16, ctypes.byref(v)) == _lib.SEGB_ERR_VALUE
+    assert "at least one layer" in _lib.last_error()
+    arr = (ctypes.c_void_p * 2)(None, None)
+    assert lib.segb_stack_workspace_bytes(arr, 2, 1, 4, 4, _lib.BF16, ctypes.byref(v)) == _lib.SEGB_ERR_VALUE
+    assert lib.segb_stack_forward(arr, 2, None, 0, 1, 4, 4, None, 0, 0, None, 0, None) == _lib.SEGB_ERR_VALUE
+    assert lib.segb_stack_forward(arr, 2, None, 0, 0, 4, 4, None, 0, 0, None, 0, None) == _lib.SEGB_ERR_SHAPE
