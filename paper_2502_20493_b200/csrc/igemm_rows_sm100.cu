@@ -626,6 +626,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
             char *pc = reinterpret_cast<char *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE + cw0) * plane_b +
                        (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co, row, col 2j)
+            // 8-byte store pointer: even position of this lane's pair, channel + (lane & 1)
+            const int odd = lane & 1;
+            char *pc2 = pc - odd * 4 + odd * plane_b;
             // CH channels per TMEM load per class; the next chunk's loads are in flight while
             // this chunk is converted and stored
             constexpr int CH = kEpiChunk;
@@ -655,22 +658,38 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     __syncwarp();
                     if (lane == 0) release_acc(acc);
                 }
+                // Stores of 8 B per lane: lanes 2j and 2j+1 (adjacent positions) swap one bf16x2
+                // pair per channel pair, so the even lane holds positions 2j, 2j+1 of channel k
+                // and the odd lane the same positions of channel k+1 (a warp instruction writes
+                // two 128-byte row segments). With 4-byte stores four warps per SM cap HBM
+                // writes at ~4.9 TB/s; 8-byte ones reach ~6.2 TB/s (tools/probes/store_width_probe.cu).
 #pragma unroll
-                for (int k = 0; k < CH; ++k) {
-                    if (RS != 2) {  // class index c = 2r + s; each store is the (even, odd) column pair
-                        const uint32_t row0 = pack_bf16x2(__uint_as_float(cur[2 * RE + SE][k]),
-                                                          __uint_as_float(cur[2 * RE + (1 - SE)][k]));
-                        const uint32_t row1 = pack_bf16x2(__uint_as_float(cur[2 * (1 - RE) + SE][k]),
-                                                          __uint_as_float(cur[2 * (1 - RE) + (1 - SE)][k]));
-                        if (lane_active && !(ABL(1))) {
-                            *reinterpret_cast<uint32_t *>(pc) = row0;
-                            *reinterpret_cast<uint32_t *>(pc + ow_b) = row1;
+                for (int k = 0; k < CH; k += 2) {
+                    uint32_t mine[2], sent[2];  // [output row]: bf16x2 of channel k + odd (kept), k + !odd (sent)
+                    if (RS != 2) {  // class index c = 2r + s; a bf16x2 is the (even, odd) column pair
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk) {
+                            const uint32_t r0 = pack_bf16x2(__uint_as_float(cur[2 * RE + SE][k + kk]),
+                                                            __uint_as_float(cur[2 * RE + (1 - SE)][k + kk]));
+                            const uint32_t r1 = pack_bf16x2(__uint_as_float(cur[2 * (1 - RE) + SE][k + kk]),
+                                                            __uint_as_float(cur[2 * (1 - RE) + (1 - SE)][k + kk]));
+                            if (kk == odd) { mine[0] = r0; mine[1] = r1; } else { sent[0] = r0; sent[1] = r1; }
                         }
                     } else {  // TMEM slot = column parity s
-                        const uint32_t row = pack_bf16x2(__uint_as_float(cur[SE][k]), __uint_as_float(cur[1 - SE][k]));
-                        if (lane_active && !(ABL(1))) *reinterpret_cast<uint32_t *>(pc) = row;
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk) {
+                            const uint32_t r0 = pack_bf16x2(__uint_as_float(cur[SE][k + kk]),
+                                                            __uint_as_float(cur[1 - SE][k + kk]));
+                            if (kk == odd) mine[0] = r0; else sent[0] = r0;
+                        }
                     }
-                    pc += plane_b;
+#pragma unroll
+                    for (int rr = 0; rr < (RS != 2 ? 2 : 1); ++rr) {
+                        const uint32_t got = __shfl_xor_sync(0xffffffffu, sent[rr], 1);
+                        const uint2 v = odd ? make_uint2(got, mine[rr]) : make_uint2(mine[rr], got);
+                        if (lane_active && !(ABL(1))) *reinterpret_cast<uint2 *>(pc2 + rr * ow_b) = v;
+                    }
+                    pc2 += 2 * plane_b;
                 }
             };
             for (int co0 = 0; co0 < NEW; co0 += 2 * CH) {
