@@ -49,6 +49,10 @@ constexpr int kRowsEpw = SEGB_ROWS_EPW;
 constexpr int kLoaderWarp0 = 2 + kRowsEpw;                   // first of the 4 row-loader warps
 constexpr int kRowsThreads = (kLoaderWarp0 + 4) * 32;        // weights, MMA, epilogue, loaders
 constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
+#ifndef SEGB_ROWS_LOAD_BUFS
+#define SEGB_ROWS_LOAD_BUFS 3
+#endif
+constexpr int kLoadBufs = SEGB_ROWS_LOAD_BUFS;  // input-row units in flight per loader thread
 
 struct RowsClass {
     int st_r, st_s, base_r, base_s, tap0;
@@ -443,16 +447,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (++ul == nr && ++ut < t1) ul = nr - loads_of(ut);
             }
         };
-        // three register buffers in rotation, the loop unrolled by three so that no buffer is
-        // ever copied: a unit's loads are issued three units before its slot stores consume them
+        // kLoadBufs register buffers in rotation, the loop unrolled by as many so that no buffer
+        // is ever copied: a unit's loads are issued kLoadBufs units before its slot stores
+        // consume them
         // (a `cur = nxt` rotation of register arrays made every iteration wait for the loads it
         // had just issued: one full memory latency per unit)
-        uint4 rb[3][8], hb[3];
-        int bkb[3];     // channel block of the unit in each buffer
-        bool bv[3];     // buffer holds a unit
+        uint4 rb[kLoadBufs][8], hb[kLoadBufs];
+        int bkb[kLoadBufs];     // channel block of the unit in each buffer
+        bool bv[kLoadBufs];     // buffer holds a unit
         int ct = t0, cl = t0 < t1 ? nr - loads_of(t0) : 0, ckb_ = 0;  // next unit to load
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < kLoadBufs; ++k) {
             bv[k] = ct < t1;
             bkb[k] = ckb_;
             if (bv[k]) {
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         bool more = bv[0];
         while (more) {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
+            for (int k = 0; k < kLoadBufs; ++k) {
                 if (!bv[k]) {
                     more = false;
                     break;
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (PAIRKB || ckb == KBC - 1) {
                     if (++qs == (uint32_t)ring) { qs = 0; qph ^= 1; }
                 }
-                // refill this buffer with the unit three ahead
+                // refill this buffer with the unit kLoadBufs ahead
                 bv[k] = ct < t1;
                 bkb[k] = ckb_;
                 if (bv[k]) {
