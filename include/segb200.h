@@ -139,6 +139,14 @@ int segb_stack_forward(const segb_layer *const *layers, int count, const void *x
  * splitmix64(seed + i)) * 2^-64), optionally rounded on to bf16. */
 int segb_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, void *stream);
 
+/* Dataset images to the device (tensor_io.py:27-52 parse_ppm).
+ * src: device (images, height, width, channels) u8, the interleaved PPM payload;
+ * dst: device (images, channels, height, width) of dst_dtype with
+ * dst = float32(src) / float32(255) (IEEE fp32 division, bitwise the reference's
+ * decode; bf16 rounds that value, f64 widens it). */
+int segb_u8_hwc_to_chw(const void *src, int64_t images, int height, int width, int channels, void *dst,
+                       int dst_dtype, void *stream);
+
 /* number of kernels this library has launched since load (evidence counter) */
 int64_t segb_launch_count(void);
 

@@ -41,6 +41,7 @@ SIGNATURES = {
     "segb_workspace_high_water": (_i, [_i, _i, ctypes.POINTER(_i64)]),
     "segb_stack_workspace_bytes": (_i, [ctypes.POINTER(_p), _i, _i64, _i, _i, _i, ctypes.POINTER(_i64)]),
     "segb_stack_forward": (_i, [ctypes.POINTER(_p), _i, _p, _i, _i64, _i, _i, _p, _i, _i, _p, _i64, _p]),
+    "segb_u8_hwc_to_chw": (_i, [_p, _i64, _i, _i, _i, _p, _i, _p]),
 }
 
 _lib = None

@@ -544,6 +544,10 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     if (!nt)
         for (int cand : {256, 128, 64, 32})
             if (cand <= nmax && cop % cand == 0) { nt = cand; break; }
+    if (const char *e = getenv("SEGB200_K3_NTILE")) {  // A/B experiments: force the N tile
+        const int v = atoi(e);
+        if (v >= 32 && v <= nmax && v % 32 == 0 && cop % v == 0) nt = v;
+    }
     if (nt % 32 || nt > nmax) return false;
     prm.n_tile = nt;
     prm.n_blocks = cop / nt;

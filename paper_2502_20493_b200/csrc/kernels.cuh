@@ -18,4 +18,8 @@ int run_prep_gemm_tf32(const void *bank, int bank_dtype, int c_in, int c_in_pad,
 // synthetic inputs (synth.cu)
 int run_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, cudaStream_t st);
 
+// dataset images (image_io.cu)
+int run_u8_hwc_to_chw(const void *src, int64_t images, int height, int width, int channels, void *dst,
+                      int dst_dtype, cudaStream_t st);
+
 }  // namespace segb

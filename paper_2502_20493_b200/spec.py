@@ -83,6 +83,12 @@ def mult_count_segregated(spec: TransposeConvSpec) -> int:
     return int(v)
 
 
+def mult_count_reference(spec: TransposeConvSpec) -> int:
+    """analysis.py:40-43: multiplications of the reference engine (Alg. 1), M_h*M_w*n^2*c_in*c_out."""
+    oh, ow = output_dims(spec)
+    return oh * ow * spec.kernel_n ** 2 * spec.c_in * spec.c_out
+
+
 def algorithmic_bytes(spec: TransposeConvSpec, batch: int, x_bytes: int, y_bytes: int,
                       w_bytes: int) -> int:
     """in + out + weights, each touched once (no upsampled or padded buffer)."""
