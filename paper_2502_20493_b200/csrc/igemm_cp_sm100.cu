@@ -169,7 +169,10 @@ __global__ void __launch_bounds__(kCpThreads, 1)
                         const uint32_t idesc = both ? idesc2 : idesc1;
                         const bool fresh = u == 0 && w.fresh;
                         for (int kb = 0; kb < prm.k_cblocks; ++kb) {
-                            mbar_wait_cluster(&full[stage], phase);
+                            // CTA-scope acquire: the stage is filled by TMA (async proxy) only,
+                            // both CTAs' bytes completing on this barrier; a cluster-scope acquire
+                            // here invalidated L1 (CCTL.IVALL) once per stage
+                            mbar_wait(&full[stage], phase);
                             tc_fence_after();
                             const uint32_t a0 = aLo0 + stage * (a_bytes >> 4), b0 = bLo0 + stage * (b_cta >> 4);
 #pragma unroll

@@ -553,7 +553,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
                 for (int kb = 0; kb < KBC; ++kb)
                     if (!(ABL(64))) {
+#ifdef SEGB_ROWS_SLOT_CTA_SCOPE
+                        if (TWO) mbar_wait(&slot_full[s * KBC + kb], ph);
+#else
                         if (TWO) mbar_wait_cluster(&slot_full[s * KBC + kb], ph);
+#endif
                         else mbar_wait(&slot_full[s * KBC + kb], ph);
                     }
             }
