@@ -334,8 +334,15 @@ __global__ void __launch_bounds__(256) reference_engine_kernel(DirectArgs a, int
 
 template <typename TX, typename TC, typename TY, bool RBF, int N, int COB>
 int launch_direct_n(const DirectArgs &a, cudaStream_t st) {
-    constexpr int RQ = (N <= 5) ? 4 : 2;
-    constexpr int CQ = (N <= 5 && COB <= 2 && sizeof(TC) == 4) ? 2 : 1;  // column quads per thread
+#ifndef SEGB_DIRECT_RQ
+#define SEGB_DIRECT_RQ 0
+#endif
+#ifndef SEGB_DIRECT_CQ
+#define SEGB_DIRECT_CQ 0
+#endif
+    // row / column quads per thread (SEGB_DIRECT_RQ / _CQ override them for A/B builds)
+    constexpr int RQ = SEGB_DIRECT_RQ > 0 ? SEGB_DIRECT_RQ : ((N <= 5) ? 4 : 2);
+    constexpr int CQ = SEGB_DIRECT_CQ > 0 ? SEGB_DIRECT_CQ : ((N <= 5 && COB <= 2 && sizeof(TC) == 4) ? 2 : 1);
     dim3 block(32, kDirectRowsPerBlock);
     const int64_t nco_blk = ceil_div(a.c_out, COB);
     const int64_t nrb = ceil_div(a.nqr, kDirectRowsPerBlock * RQ);
