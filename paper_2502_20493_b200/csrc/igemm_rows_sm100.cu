@@ -29,8 +29,8 @@
 //     output rows with coalesced 4-byte stores (128 B per warp instruction),
 //     the next channels' TMEM loads in flight; every output element written once.
 //
-// Warps: 0 weight TMA, 1 MMA issuer (+TMEM owner), 2..9 epilogue (TMEM lane
-// quarter warp % 4, channel half (warp - 2) / 4), 10..13 row loaders / transposers.
+// Warps: 0 weight TMA, 1 MMA issuer (+TMEM owner), 2..3 idle, 4..7 epilogue (TMEM lane
+// quarters), 8..11 row loaders / transposers (registers rebalanced, see kRegsLoad).
 #include <cstdlib>
 #include <mutex>
 
@@ -40,14 +40,16 @@
 namespace segb {
 
 static unsigned long long *g_rows_prof_buf = nullptr;
-// epilogue warps: 8 = two per TMEM lane quarter, each storing half of the output channels
-// (twice the TMEM loads and stores in flight of 4 warps)
-#ifndef SEGB_ROWS_EPW
-#define SEGB_ROWS_EPW 4
-#endif
-constexpr int kRowsEpw = SEGB_ROWS_EPW;
-constexpr int kLoaderWarp0 = 2 + kRowsEpw;                   // first of the 4 row-loader warps
-constexpr int kRowsThreads = (kLoaderWarp0 + 4) * 32;        // weights, MMA, epilogue, loaders
+constexpr int kRowsEpw = 4;  // epilogue warps, one per TMEM lane quarter (8 measured slower: spills)
+// Three warpgroups with rebalanced registers (setmaxnreg): warpgroup 0 = weight TMA (warp 0),
+// MMA issuer (warp 1), two idle warps, shrunk to kRegsCtl registers; warpgroup 1 = the four
+// epilogue warps (TMEM lane quarter warp % 4), kept at the launch budget; warpgroup 2 = the
+// four row loaders, grown to kRegsLoad registers so each thread can keep up to 5 input units in
+// flight (SEGB_ROWS_LOAD_BUFS; measured: 3 is as fast as 4 or 5 on l6/l7).
+constexpr int kEpiWarp0 = 4;
+constexpr int kLoaderWarp0 = 8;                               // first of the 4 row-loader warps
+constexpr int kRowsThreads = 12 * 32;                         // launch budget: 168 registers
+constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168 + 232) <= 64 K
 constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
 #ifndef SEGB_ROWS_LOAD_BUFS
 #define SEGB_ROWS_LOAD_BUFS 3
@@ -384,14 +386,96 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const int t1 = min(TWO ? prm.half_tiles : prm.total_tiles, t0 + prm.tiles_per_cta);
     auto loads_of = [&](int t) { return (t == t0 || (t % prm.rows) == 0) ? nr : 1; };
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- the resident weights, in schedule order
-            if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank, COSPLIT);
-            else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
-            else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
-            else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
-        }
+    // setmaxnreg at the top of each warpgroup's branch (all four warps execute it, and it
+    // dominates the code it budgets for)
+    if (warp < kEpiWarp0) {
+#ifndef SEGB_ROWS_NO_SETMAXNREG
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+#endif
+        if (warp == 0) {
+            if (lane == 0) {  // ---------------- the resident weights, in schedule order
+                if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank, COSPLIT);
+                else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
+                else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
+                else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
+            }
+        } else if (warp == 1) {
+            // ---------------- MMA issuer (TWO: the leader CTA issues for the pair)
+            if (!(TWO && rank != 0)) {  // (the peer's MMA warp idles)
+            if (TWO) mbar_wait_cluster(b_full, 0);
+            else mbar_wait(b_full, 0);
+            const uint32_t aLo0 = desc_lo_sw128(smem_u32(sRing)), bLo0 = desc_lo_sw128(smem_u32(sB));
+            const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
+            const uint32_t leader = elect_one();
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            // ring cursor of the first window row of the current tile (slot, phase) and the tile's
+            // row in its strip, all advanced incrementally: no runtime division in this loop, so
+            // ptxas keeps the slot and descriptor arithmetic in uniform registers (a `% ring` here
+            // went through F2I in vector registers and cost an R2UR per MMA operand)
+            uint32_t sq = 0, phq = 0;
+            int ri = t0 % prm.rows;
+            long long pt_ = clock64();
+            for (int t = t0; t < t1; ++t) {
+                ROWS_PROF(2, pt_)
+                if (!(ABL(32))) {
+                    if (TWO) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                    else mbar_wait(&tempty[acc], acc_phase ^ 1);
+                }
+                ROWS_PROF(0, pt_)
+                for (int l = 0; l < nr; ++l) {
+                    uint32_t s = sq + l, ph = phq;
+                    if (s >= (uint32_t)ring) { s -= ring; ph ^= 1; }
+    #pragma unroll
+                    for (int kb = 0; kb < KBC; ++kb)
+                        if (!(ABL(64))) {
+    #ifdef SEGB_ROWS_SLOT_CTA_SCOPE
+                            if (TWO) mbar_wait(&slot_full[s * KBC + kb], ph);
+    #else
+                            if (TWO) mbar_wait_cluster(&slot_full[s * KBC + kb], ph);
+    #endif
+                            else mbar_wait(&slot_full[s * KBC + kb], ph);
+                        }
+                }
+                tc_fence_after();
+                ROWS_PROF(1, pt_)
+                const uint32_t d0 = tmem_base + acc * NCL * (COSPLIT ? N / 2 : N);
+                if (ABL(4)) {
+                } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+                else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+                else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+                else issue_tile<NH, KBC, SWAP, MR, 1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+                // commits, branch-free like the MMAs (lane `leader` issues them)
+                if (!(ABL(32))) {
+                    if (TWO) tc_commit_2sm_mc_pred(&tfull[acc], 3, leader);
+                    else tc_commit_pred(&tfull[acc], leader);
+                }
+                // release input rows no later tile of this strip reads, advance the window
+                const int ri_next = ri + 1 == prm.rows ? 0 : ri + 1;
+                const bool cont = (t + 1 < t1) && ri_next != 0;
+                const int nrel = cont ? 1 : nr;
+                for (int l = 0; l < nrel; ++l) {
+                    uint32_t s = sq + l;
+                    if (s >= (uint32_t)ring) s -= ring;
+    #pragma unroll
+                    for (int kb = 0; kb < KBC; ++kb)
+                        if (!(ABL(64))) {
+                            if (TWO) tc_commit_2sm_mc_pred(&slot_empty[s * KBC + kb], 3, leader);
+                            else tc_commit_pred(&slot_empty[s * KBC + kb], leader);
+                        }
+                }
+                sq += nrel;
+                if (sq >= (uint32_t)ring) { sq -= ring; phq ^= 1; }
+                ri = ri_next;
+                __syncwarp();
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            }
+        }  // warps 2, 3: idle (they only take part in warpgroup 0's register release)
     } else if (warp >= kLoaderWarp0) {
+#ifndef SEGB_ROWS_NO_SETMAXNREG
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsLoad));
+#endif
         // ---------------- row loaders / transposers: NCHW input row (64 channels x MR columns
         // + halo) -> K-major SWIZZLE_128B slot rows. Thread (cg = t & 7, cc = t >> 3) loads 8
         // channels x 8 columns with 128-bit loads (coalesced along the row), transposes the 8x8
@@ -523,80 +607,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
             }
         }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer (TWO: the leader CTA issues for the pair)
-        if (!(TWO && rank != 0)) {  // (the peer's MMA warp idles)
-        if (TWO) mbar_wait_cluster(b_full, 0);
-        else mbar_wait(b_full, 0);
-        const uint32_t aLo0 = desc_lo_sw128(smem_u32(sRing)), bLo0 = desc_lo_sw128(smem_u32(sB));
-        const uint32_t S16 = prm.slot_bytes >> 4, B16 = prm.b_tile_bytes >> 4;
-        const uint32_t leader = elect_one();
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        // ring cursor of the first window row of the current tile (slot, phase) and the tile's
-        // row in its strip, all advanced incrementally: no runtime division in this loop, so
-        // ptxas keeps the slot and descriptor arithmetic in uniform registers (a `% ring` here
-        // went through F2I in vector registers and cost an R2UR per MMA operand)
-        uint32_t sq = 0, phq = 0;
-        int ri = t0 % prm.rows;
-        long long pt_ = clock64();
-        for (int t = t0; t < t1; ++t) {
-            ROWS_PROF(2, pt_)
-            if (!(ABL(32))) {
-                if (TWO) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
-                else mbar_wait(&tempty[acc], acc_phase ^ 1);
-            }
-            ROWS_PROF(0, pt_)
-            for (int l = 0; l < nr; ++l) {
-                uint32_t s = sq + l, ph = phq;
-                if (s >= (uint32_t)ring) { s -= ring; ph ^= 1; }
-#pragma unroll
-                for (int kb = 0; kb < KBC; ++kb)
-                    if (!(ABL(64))) {
-#ifdef SEGB_ROWS_SLOT_CTA_SCOPE
-                        if (TWO) mbar_wait(&slot_full[s * KBC + kb], ph);
-#else
-                        if (TWO) mbar_wait_cluster(&slot_full[s * KBC + kb], ph);
-#endif
-                        else mbar_wait(&slot_full[s * KBC + kb], ph);
-                    }
-            }
-            tc_fence_after();
-            ROWS_PROF(1, pt_)
-            const uint32_t d0 = tmem_base + acc * NCL * (COSPLIT ? N / 2 : N);
-            if (ABL(4)) {
-            } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
-            else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
-            else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
-            else issue_tile<NH, KBC, SWAP, MR, 1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
-            // commits, branch-free like the MMAs (lane `leader` issues them)
-            if (!(ABL(32))) {
-                if (TWO) tc_commit_2sm_mc_pred(&tfull[acc], 3, leader);
-                else tc_commit_pred(&tfull[acc], leader);
-            }
-            // release input rows no later tile of this strip reads, advance the window
-            const int ri_next = ri + 1 == prm.rows ? 0 : ri + 1;
-            const bool cont = (t + 1 < t1) && ri_next != 0;
-            const int nrel = cont ? 1 : nr;
-            for (int l = 0; l < nrel; ++l) {
-                uint32_t s = sq + l;
-                if (s >= (uint32_t)ring) s -= ring;
-#pragma unroll
-                for (int kb = 0; kb < KBC; ++kb)
-                    if (!(ABL(64))) {
-                        if (TWO) tc_commit_2sm_mc_pred(&slot_empty[s * KBC + kb], 3, leader);
-                        else tc_commit_pred(&slot_empty[s * KBC + kb], leader);
-                    }
-            }
-            sq += nrel;
-            if (sq >= (uint32_t)ring) { sq -= ring; phq ^= 1; }
-            ri = ri_next;
-            __syncwarp();
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-        }
     } else {
-        // ---------------- epilogue (warps 2..): warp reads TMEM lane quarter warp % 4. The
+        // ---------------- epilogue (warps 4..7): warp reads TMEM lane quarter warp % 4. The
         // classes of a position are in registers, so each lane writes the pair of output
         // columns (2j, 2j+1) of each of its output rows as one 4-byte bf16x2 store: a warp
         // store covers 128 (M=64: 64) contiguous bytes of one output row, every output element
@@ -609,9 +621,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const bool lane_active = COSPLIT || MR == 128 || lane < 16;
         const int NE = COSPLIT ? N / 2 : N;              // TMEM columns (= output channels) per class here
         const int chalf = COSPLIT ? (quarter >> 1) : 0;  // this warp's output-channel half
-        // kRowsEpw = 8: the two warps of a lane quarter split the NE channels of each class
-        const int NEW = NE / (kRowsEpw / 4);             // channels per class this warp stores
-        const int cw0 = ((warp - 2) / 4) * NEW;          // its first channel (TMEM column)
+        const int NEW = NE, cw0 = 0;  // channels per class this warp stores, its first one
         auto release_acc = [&](int a) {
             if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
             else mbar_arrive(&tempty[a]);
@@ -631,7 +641,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             long long pe_ = clock64();
             if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            if (warp == 2) { ROWS_PROF(3, pe_) }
+            if (warp == kEpiWarp0) { ROWS_PROF(3, pe_) }
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
             char *pc = reinterpret_cast<char *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE + cw0) * plane_b +
                        (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co, row, col 2j)
@@ -705,10 +715,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 chunk(co0, v, v2);
                 if (co0 + CH < NEW) chunk(co0 + CH, v2, v);
             }
-            if (warp == 2) { ROWS_PROF(4, pe_) }
+            if (warp == kEpiWarp0) { ROWS_PROF(4, pe_) }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-    }
+        }
     tc_fence_before();
     __syncthreads();
     if (TWO) cluster_sync_all();  // the leader's MMAs write this CTA's TMEM until both are done
