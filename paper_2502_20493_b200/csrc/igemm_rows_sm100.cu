@@ -179,7 +179,7 @@ __host__ __device__ inline RowsSmem rows_layout(const RowsParams &p, int ntaps, 
     s.b = 0;
     s.ring = s.b + ntaps * kbc * p.b_tile_bytes;
     s.bars = s.ring + p.ring * kbc * p.slot_bytes;
-    s.total = s.bars + (1 + 2 * p.ring * kbc + 4) * 8 + 16;
+    s.total = s.bars + (1 + 2 * p.ring * kbc + 8) * 8 + 16;  // b_full, slots, 4 tfull + 4 tempty, TMEM addr
     return s;
 }
 
@@ -320,7 +320,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const RowsParams prm) {
     constexpr bool TWO = RS == 3 || RS == 4;  // 2-SM pair: M = 128 (RS 3, MR 64) or 256 (RS 4, MR 128)
     constexpr bool COSPLIT = RS == 3;
-    constexpr int NCL = RS == 2 ? 2 : 4;  // parity classes per CTA
+    // RS = 5 (HALF): one CTA, every tile issued as two row-parity halves (schedules RSEL 0, 1)
+    // into four half-tile TMEM buffers, so the epilogue drains row 2i while the MMAs of row
+    // 2i+1 run and the next tile's first half can start as soon as a half buffer is free
+    constexpr bool HALF = RS == 5;
+    constexpr int NCL = (RS == 2 || HALF) ? 2 : 4;  // parity classes per accumulator buffer
+    constexpr int NBUF = HALF ? 4 : 2;              // TMEM accumulator buffers
     // M = 64 rows with two channel blocks: loader warps 0-1 fill block 0, warps 2-3 block 1 of
     // the same input row at once (else each unit is one (row, block) filled by all four)
     constexpr bool PAIRKB = MR == 64 && KBC == 2;
@@ -328,10 +333,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int rsel = RS == 2 ? (int)(blockIdx.x % 2) : -1;
-    const int cta = blockIdx.x / (RS == 1 ? 1 : 2);
+    const int cta = blockIdx.x / ((RS == 1 || HALF) ? 1 : 2);
     const int rank = TWO ? (int)cluster_ctarank() : 0;
     const int toff = TWO ? rank * prm.half_tiles : 0;  // tile index offset of this CTA's batch half
-    const int ntiles_b = NCL * NH * NH;
+    const int ntiles_b = (RS == 2 ? 2 : 4) * NH * NH;  // resident B tiles
     const RowsSmem L = rows_layout(prm, ntiles_b, KBC);
     uint8_t *sB = smem + L.b;
     uint8_t *sRing = smem + L.ring;
@@ -340,8 +345,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const int ring = prm.ring;
     uint64_t *slot_empty = slot_full + ring * KBC;
     uint64_t *tfull = slot_empty + ring * KBC;
-    uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *tempty = tfull + NBUF;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NBUF);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int N = prm.c_out;
@@ -351,19 +356,19 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const int nr = RS == 2 ? NH : prm.nr;
 
     if (threadIdx.x == 0) {
-        mbar_init(b_full, 1);
+        mbar_init(b_full, HALF ? 2 : 1);  // HALF: the two schedules' weights, two expect_tx
         for (int i = 0; i < ring * KBC; ++i) {
             mbar_init(&slot_full[i], (PAIRKB ? 2 : 4) * CG);  // one arrival per loader warp filling the slot
             mbar_init(&slot_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NBUF; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], kRowsEpw * CG);  // one arrival per epilogue warp (TWO: of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     }
-    const uint32_t tcols = tmem_pow2(2 * NCL * N / (COSPLIT ? 2 : 1));  // 2 buffers x NCL classes x N (RS 3: N/2)
+    const uint32_t tcols = tmem_pow2(NBUF * NCL * N / (COSPLIT ? 2 : 1));  // buffers x NCL classes x N (RS 3: N/2)
     if (warp == 1) {
         if (TWO) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -396,7 +401,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             if (lane == 0) {  // ---------------- the resident weights, in schedule order
                 if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank, COSPLIT);
                 else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
-                else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
+                else if (HALF) {  // both row parities' schedules, the second after the first's tiles
+                    load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
+                    load_weights<NH, KBC, SWAP, 1>(sB + make_schedule<NH, SWAP, 0>().ntiles * KBC * prm.b_tile_bytes,
+                                                   &tmB, b_full, prm);
+                } else if (rsel == 0) load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
                 else load_weights<NH, KBC, SWAP, 1>(sB, &tmB, b_full, prm);
             }
         } else if (warp == 1) {
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             long long pt_ = clock64();
             for (int t = t0; t < t1; ++t) {
                 ROWS_PROF(2, pt_)
-                if (!(ABL(32))) {
+                if (!HALF && !(ABL(32))) {
                     if (TWO) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                     else mbar_wait(&tempty[acc], acc_phase ^ 1);
                 }
@@ -440,13 +449,29 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 tc_fence_after();
                 ROWS_PROF(1, pt_)
                 const uint32_t d0 = tmem_base + acc * NCL * (COSPLIT ? N / 2 : N);
-                if (ABL(4)) {
+                if constexpr (HALF) {  // two half tiles: row parity h into its own TMEM buffer
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (!(ABL(32))) mbar_wait(&tempty[acc], acc_phase ^ 1);
+                        tc_fence_after();
+                        // class row parity h reads the union window from row offset dminr_rs[h] - dmin_r
+                        uint32_t sqh = sq + (uint32_t)(prm.dminr_rs[h] - prm.dmin_r);
+                        if (sqh >= (uint32_t)ring) sqh -= ring;
+                        const uint32_t dh = tmem_base + acc * NCL * N;
+                        const uint32_t bh = bLo0 + (uint32_t)(h * make_schedule<NH, SWAP, 0>().ntiles * KBC) * B16;
+                        if (ABL(4)) {
+                        } else if (h == 0) issue_tile<NH, KBC, SWAP, MR, 0>(dh, aLo0, bh, sqh, ring, S16, B16, N, leader);
+                        else issue_tile<NH, KBC, SWAP, MR, 1>(dh, aLo0, bh, sqh, ring, S16, B16, N, leader);
+                        if (!(ABL(32))) tc_commit_pred(&tfull[acc], leader);
+                        if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+                    }
+                } else if (ABL(4)) {
                 } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
                 else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
                 else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
                 else issue_tile<NH, KBC, SWAP, MR, 1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
                 // commits, branch-free like the MMAs (lane `leader` issues them)
-                if (!(ABL(32))) {
+                if (!HALF && !(ABL(32))) {
                     if (TWO) tc_commit_2sm_mc_pred(&tfull[acc], 3, leader);
                     else tc_commit_pred(&tfull[acc], leader);
                 }
@@ -468,7 +493,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (sq >= (uint32_t)ring) { sq -= ring; phq ^= 1; }
                 ri = ri_next;
                 __syncwarp();
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (!HALF && ++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
             }
         }  // warps 2, 3: idle (they only take part in warpgroup 0's register release)
@@ -634,17 +659,21 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const int row_off = RS == 2 ? (rsel != RE ? 1 : 0) : 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = t0; t < t1; ++t) {
+        constexpr int HT = HALF ? 2 : 1;  // accumulator buffers (half tiles) per tile
+        for (int u = t0 * HT; u < t1 * HT; ++u) {
+            const int t = u / HT;
             const int ta = t + toff;
             const int i = ta % prm.rows, rest = ta / prm.rows;
             const int ms = rest % prm.msub, b = rest / prm.msub;
+            // HALF: buffer u holds the classes of row parity u % 2 -> output row 2i + (h != RE)
+            const int row_h = HALF ? ((u & 1) != RE ? 1 : 0) : row_off;
             long long pe_ = clock64();
             if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (warp == kEpiWarp0) { ROWS_PROF(3, pe_) }
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
             char *pc = reinterpret_cast<char *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE + cw0) * plane_b +
-                       (int64_t)(2 * i + row_off) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co, row, col 2j)
+                       (int64_t)(2 * i + row_h) * ow_b + (int64_t)(ms * 2 * MR + 2 * m) * 2;  // (co, row, col 2j)
             // 8-byte store pointer: even position of this lane's pair, channel + (lane & 1)
             const int odd = lane & 1;
             char *pc2 = pc - odd * 4 + odd * plane_b;
@@ -656,7 +685,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0 && !(ABL(32))) release_acc(acc);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
                 continue;
             }
 #pragma unroll
@@ -685,7 +714,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
                 for (int k = 0; k < CH; k += 2) {
                     uint32_t mine[2], sent[2];  // [output row]: bf16x2 of channel k + odd (kept), k + !odd (sent)
-                    if (RS != 2) {  // class index c = 2r + s; a bf16x2 is the (even, odd) column pair
+                    if (RS != 2 && !HALF) {  // class index c = 2r + s; a bf16x2 is the (even, odd) column pair
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
                             const uint32_t r0 = pack_bf16x2(__uint_as_float(cur[2 * RE + SE][k + kk]),
@@ -703,7 +732,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         }
                     }
 #pragma unroll
-                    for (int rr = 0; rr < (RS != 2 ? 2 : 1); ++rr) {
+                    for (int rr = 0; rr < (RS != 2 && !HALF ? 2 : 1); ++rr) {
                         const uint32_t got = __shfl_xor_sync(0xffffffffu, sent[rr], 1);
                         const uint2 v = odd ? make_uint2(got, mine[rr]) : make_uint2(mine[rr], got);
                         if (lane_active && !(ABL(1))) *reinterpret_cast<uint2 *>(pc2 + rr * ow_b) = v;
@@ -716,7 +745,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (co0 + CH < NEW) chunk(co0 + CH, v2, v);
             }
             if (warp == kEpiWarp0) { ROWS_PROF(4, pe_) }
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
         }
         }
     tc_fence_before();
@@ -803,7 +832,12 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
         const int ring_min = std::max(4, nr_cta);
         for (prm.ring = kRingMax; prm.ring > ring_min; --prm.ring)
             if (rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024 <= 227 * 1024) break;
-        if (rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024 <= 227 * 1024) return true;
+        if (rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024 <= 227 * 1024) {
+            // SEGB200_ROWS_HALF=1: one CTA per strip with half-tile TMEM buffers (kernel RS = 5)
+            const char *hv = getenv("SEGB200_ROWS_HALF");
+            if (nsplit == 1 && nh == 2 && hv && atoi(hv)) nsplit = 5;
+            return true;
+        }
     }
     return false;
 }
@@ -813,6 +847,7 @@ static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit) {
     if (nsplit == 3) return mr == 64 && nh == 2;
     if (nsplit == 4) return mr == 128 && nh == 2;
     if (mr == 128 && nsplit == 1) return true;
+    if (nsplit == 5) return mr == 128 && nh == 2;
     if (mr == 128 && nsplit == 2) return nh == 2 && kbc == 2 && swap == 0;
     if (mr == 64 && nh == 2 && swap == 0) return true;
     return mr == 64 && nh == 2 && kbc == 2 && swap == 1 && nsplit == 2;
@@ -829,7 +864,7 @@ template <int NH, int KBC, int SWAP, int MR, int NS>
 static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const RowsParams &prm) {
     auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (NS < 3) {
+    if (NS < 3 || NS == 5) {
         kern<<<grid, kRowsThreads, smem, st>>>(tmB, prm);
         return;
     }
@@ -858,7 +893,7 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     {
         cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
         cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out_pad * s.c_in_pad * 2};
-        cuuint32_t box[3] = {64, (cuuint32_t)(nsplit >= 3 ? s.c_out / 2 : s.c_out), 1};
+        cuuint32_t box[3] = {64, (cuuint32_t)((nsplit == 3 || nsplit == 4) ? s.c_out / 2 : s.c_out), 1};
         cuuint32_t es[3] = {1, 1, 1};
         CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -886,16 +921,17 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid;
     size_t smem;
-    if (nsplit >= 3) {  // CTA pairs over the two batch halves
+    if (nsplit == 3 || nsplit == 4) {  // CTA pairs over the two batch halves
         const int strips = (int)std::min<int64_t>(prm.half_tiles, sms / 2);
         grid = 2 * strips;
         prm.tiles_per_cta = (int)ceil_div(prm.half_tiles, strips);
         smem = rows_layout(prm, 4 * nh * nh, kbc).total + 1024;
     } else {
-        const int strips = (int)std::min<int64_t>(prm.total_tiles, sms / nsplit);  // CTAs per channel slice
-        grid = strips * nsplit;
+        const int cps = nsplit == 5 ? 1 : nsplit;  // CTAs per strip
+        const int strips = (int)std::min<int64_t>(prm.total_tiles, sms / cps);  // CTAs per channel slice
+        grid = strips * cps;
         prm.tiles_per_cta = (int)ceil_div(prm.total_tiles, strips);
-        smem = rows_layout(prm, 4 / nsplit * nh * nh, kbc).total + 1024;
+        smem = rows_layout(prm, 4 / cps * nh * nh, kbc).total + 1024;
     }
     int rc = SEGB_OK;
 #define SEGB_ROWS_CASE(NH_, KBC_, SW_, MR_, NS_)                                                  \
@@ -912,7 +948,8 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     SEGB_ROWS_CASE(2, 2, 0, 64, 1) SEGB_ROWS_CASE(2, 2, 0, 64, 2) SEGB_ROWS_CASE(2, 2, 1, 64, 2)
     SEGB_ROWS_CASE(2, 1, 0, 64, 3) SEGB_ROWS_CASE(2, 2, 0, 64, 3) SEGB_ROWS_CASE(2, 1, 1, 64, 3)
     SEGB_ROWS_CASE(2, 2, 1, 64, 3) SEGB_ROWS_CASE(2, 1, 0, 128, 4) SEGB_ROWS_CASE(2, 1, 1, 128, 4)
-    SEGB_ROWS_CASE(2, 2, 0, 128, 4) SEGB_ROWS_CASE(2, 2, 1, 128, 4)
+    SEGB_ROWS_CASE(2, 2, 0, 128, 4) SEGB_ROWS_CASE(2, 2, 1, 128, 4) SEGB_ROWS_CASE(2, 1, 0, 128, 5)
+    SEGB_ROWS_CASE(2, 1, 1, 128, 5) SEGB_ROWS_CASE(2, 2, 0, 128, 5) SEGB_ROWS_CASE(2, 2, 1, 128, 5)
     { rc = fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: variant not instantiated"); }
 #undef SEGB_ROWS_CASE
     if (rc) return rc;
