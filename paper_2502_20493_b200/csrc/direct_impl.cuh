@@ -99,7 +99,10 @@ template <typename TC, int N2P> __device__ __forceinline__ void load_taps(const 
 }
 
 template <typename TX, typename TC, typename TY, bool RBF, int N, int COB, int RQ, int CQ>
-__global__ void __launch_bounds__(128) direct_kernel(DirectArgs a) {
+// one or two output channels per thread (the dataset layers): at most 80 registers so six
+// blocks fit per SM -- more warps to hide the window loads (ds512_k5 0.151 -> 0.141 ms); with
+// three channels the register cap spills and loses
+__global__ void __launch_bounds__(128, (COB <= 2 && sizeof(TC) == 4) ? 6 : 1) direct_kernel(DirectArgs a) {
     constexpr int NW = N / 2 + 1;          // input rows/cols under one output quad
     constexpr int WR = RQ + NW - 1;        // window rows for RQ row quads
     constexpr int WC = CQ + NW - 1;        // window cols for CQ column quads
