@@ -32,6 +32,7 @@ namespace {
 
 constexpr int kCpThreads = 192;  // warp 0 TMA, warp 1 MMA / forwarder, warps 2-5 epilogue
 constexpr int kCpMaxWin = 4;
+constexpr int kCpMaxStages = 12;
 
 struct CpWindow {
     int dc;     // window column offset (relative to the class grid position, before - p)
@@ -328,7 +329,11 @@ bool cp_params(const IgemmShape &s, CpParams &prm) {
     // per-class K3 with 256-wide tiles measured faster (ebgan l2-l4), so K3p takes c_out <= 128
     const int cop = (int)ceil_div(s.c_out, 32) * 32;
     if (cop > 128) return false;
-    const int nb_w = cop;
+    int nb_w = cop;
+    if (const char *e = getenv("SEGB200_K3P_NB")) {  // A/B experiments: narrower N blocks, more stages
+        const int v = atoi(e);
+        if (v >= 32 && v % 32 == 0 && cop % v == 0) nb_w = v;
+    }
     prm.nb_w = nb_w;
     prm.n_blocks = cop / nb_w;
     prm.batch = (int)s.batch; prm.c_in = s.c_in; prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
@@ -341,7 +346,7 @@ bool cp_params(const IgemmShape &s, CpParams &prm) {
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
     const int stage_bytes = kBlockM * 128 + nb_w * 128;
-    prm.stages = std::min(8, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
+    prm.stages = std::min(kCpMaxStages, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
     return prm.stages >= 2;
 }
 
