@@ -265,3 +265,34 @@ def test_k3_class_pair_tiles(monkeypatch, cp, name, h, w, ci, n, co, pad, b):
     yb = layer.forward(x, path="igemm").float().cpu().numpy()
     repb = O.compare(yb, ref, 2 ** -7, 1e-3 * float(np.abs(ref).max()))
     assert repb["passed"], (name, cp, repb)
+
+
+# K3b's opt-in variants, kept working: M=256 CTA pairs for 128-wide rows (SEGB200_ROWS_PAIR=4)
+# and K3's N tile forced to 128 run the default per-class accumulation order, so they must equal
+# the default kernel bitwise; half-tile TMEM buffers (SEGB200_ROWS_HALF=1) and the unpaired M=64
+# row split (SEGB200_ROWS_PAIR=0) accumulate each class's windows in another order, so they are
+# held to the fp32 / bf16 output gates against the default instead
+@pytest.mark.parametrize("env,val,shape,bitwise", [
+    ("SEGB200_ROWS_PAIR", "4", (128, 128, 64, 4, 64, 2, 2), True),
+    ("SEGB200_ROWS_HALF", "1", (128, 128, 64, 4, 64, 2, 2), False),
+    ("SEGB200_ROWS_HALF", "1", (64, 128, 128, 4, 32, 2, 1), False),   # 2 channel blocks, odd batch
+    ("SEGB200_ROWS_PAIR", "0", (64, 64, 128, 4, 64, 2, 2), False),   # M=64 row split: other order
+    ("SEGB200_K3_NTILE", "128", (8, 8, 256, 4, 512, 2, 4), True),
+])
+def test_opt_in_variants(monkeypatch, env, val, shape, bitwise):
+    import torch
+    h, w, ci, n, co, pad, b = shape
+    x, bank = _inputs(h, w, ci, n, co, b, 31 + h + co)
+    layer = P.prepare_layer(bank, pad, compute="bf16")
+    want = layer.forward(x, path="igemm")
+    want32 = layer.forward(x, path="igemm", out_dtype=torch.float32)
+    monkeypatch.setenv(env, val)
+    got = layer.forward(x, path="igemm")
+    got32 = layer.forward(x, path="igemm", out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    if bitwise:
+        assert torch.equal(got.view(torch.int16), want.view(torch.int16)), (env, val, shape)
+    else:
+        ref = want32.cpu().numpy().astype(np.float64)
+        assert O.compare(got32.cpu().numpy(), ref, 1e-5, 1e-6)["passed"], (env, val, shape)
+        assert O.compare(got.float().cpu().numpy(), ref, 2 ** -7, 1e-3 * float(np.abs(ref).max()))["passed"]
