@@ -108,7 +108,7 @@ struct RowsParams {
 // RSEL < 0: all four classes (du relative to the union row window);
 // RSEL = r: only the two classes of row parity r (du = tap row u).
 struct MmaGroup {
-    int du, dc, c0, nc, b0;  // window, first class, class count, first B tile
+    int du, dc, c0, nc, b0;  // window, first TMEM class slot, slot count, first B tile
 };
 template <int NH, int SWAP, int RSEL>
 struct Schedule {
@@ -118,15 +118,26 @@ struct Schedule {
     int btap[16 * 4];  // B tile k -> (class << 8) | (u << 4) | v
     bool fresh[(NH + 1) * (NH + 1) * 2];
 };
+// TMEM slot of class c = 2r + s when all four classes share a buffer: [0, 1, 3, 2] puts (0, 1)
+// next to (1, 1), so the window both row parities read with column parity 1 becomes one N = 2 c_out
+// MMA (10 instead of 11 MMAs per k-step for n = 4, P even). The permutation is its own inverse.
+#ifndef SEGB_ROWS_CLASS_PERM
+#define SEGB_ROWS_CLASS_PERM 1
+#endif
+__host__ __device__ constexpr int class_slot(int c) { return SEGB_ROWS_CLASS_PERM ? (c < 2 ? c : 5 - c) : c; }
+
 template <int NH, int SWAP, int RSEL>
 constexpr Schedule<NH, SWAP, RSEL> make_schedule() {
     Schedule<NH, SWAP, RSEL> s{};
     const int W = SWAP ? NH : NH + 1;  // distinct column windows (and row windows for RSEL < 0)
     const int DU = RSEL < 0 ? W : NH;
+    auto slot = [](int c) { return RSEL < 0 ? class_slot(c) : c; };
     int nb = 0;
-    auto add = [&](int du, int dc, int c0, int nc) {
-        s.g[s.count] = MmaGroup{du, dc, c0, nc, nb};
-        for (int c = c0; c < c0 + nc; ++c) {
+    // one MMA over TMEM slots p0 .. p0 + nc - 1 (their classes in slot order)
+    auto add = [&](int du, int dc, int p0, int nc) {
+        s.g[s.count] = MmaGroup{du, dc, p0, nc, nb};
+        for (int p = p0; p < p0 + nc; ++p) {
+            const int c = slot(p);  // the permutation is an involution
             const int r = c >> 1, q = c & 1;
             const int u = RSEL < 0 ? du - (SWAP ? 0 : r) : du, v = dc - (SWAP ? 0 : q);
             s.btap[nb++] = (c << 8) | (u << 4) | v;
@@ -151,13 +162,24 @@ constexpr Schedule<NH, SWAP, RSEL> make_schedule() {
                     else add(du, dc, 2 * RSEL, 2);
                     continue;
                 }
+                // both row parities, one column parity q: classes q and 2 + q, one MMA when
+                // their slots are adjacent
+                if (RSEL < 0 && all_r && ss[0] != ss[1]) {
+                    const int q = ss[1] ? 1 : 0;
+                    const int a = slot(q), b = slot(2 + q);
+                    if (a + 1 == b || b + 1 == a) {
+                        add(du, dc, a < b ? a : b, 2);
+                        continue;
+                    }
+                }
                 for (int r = 0; r < 2; ++r) {
                     if (!rr[r]) continue;
-                    if (ss[0] && ss[1]) {
-                        add(du, dc, 2 * r, 2);
+                    if (ss[0] && ss[1]) {  // both column parities of row r: slots adjacent either way
+                        const int a = slot(2 * r), b = slot(2 * r + 1);
+                        add(du, dc, a < b ? a : b, 2);
                     } else {
                         for (int q = 0; q < 2; ++q)
-                            if (ss[q]) add(du, dc, 2 * r + q, 1);
+                            if (ss[q]) add(du, dc, slot(2 * r + q), 1);
                     }
                 }
             }
@@ -717,10 +739,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     if (RS != 2 && !HALF) {  // class index c = 2r + s; a bf16x2 is the (even, odd) column pair
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
-                            const uint32_t r0 = pack_bf16x2(__uint_as_float(cur[2 * RE + SE][k + kk]),
-                                                            __uint_as_float(cur[2 * RE + (1 - SE)][k + kk]));
-                            const uint32_t r1 = pack_bf16x2(__uint_as_float(cur[2 * (1 - RE) + SE][k + kk]),
-                                                            __uint_as_float(cur[2 * (1 - RE) + (1 - SE)][k + kk]));
+                            constexpr int C00 = class_slot(2 * RE + SE), C01 = class_slot(2 * RE + (1 - SE));
+                            constexpr int C10 = class_slot(2 * (1 - RE) + SE), C11 = class_slot(2 * (1 - RE) + (1 - SE));
+                            const uint32_t r0 = pack_bf16x2(__uint_as_float(cur[C00][k + kk]),
+                                                            __uint_as_float(cur[C01][k + kk]));
+                            const uint32_t r1 = pack_bf16x2(__uint_as_float(cur[C10][k + kk]),
+                                                            __uint_as_float(cur[C11][k + kk]));
                             if (kk == odd) { mine[0] = r0; mine[1] = r1; } else { sent[0] = r0; sent[1] = r1; }
                         }
                     } else {  // TMEM slot = column parity s
