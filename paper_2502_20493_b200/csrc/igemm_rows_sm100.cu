@@ -454,7 +454,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     else mbar_wait(&tempty[acc], acc_phase ^ 1);
                 }
                 ROWS_PROF(0, pt_)
-                for (int l = 0; l < nr; ++l) {
+                // only the rows this tile adds: the nr - 1 it shares with the previous tile of the
+                // strip were waited for then (fewer cluster-scope acquires per tile)
+                const int lw0 = (t == t0 || ri == 0) ? 0 : nr - 1;
+                for (int l = lw0; l < nr; ++l) {
                     uint32_t s = sq + l, ph = phq;
                     if (s >= (uint32_t)ring) { s -= ring; ph ^= 1; }
     #pragma unroll
