@@ -324,21 +324,27 @@ def run_ours(args, rank, world, local_rank):
                          "upsampled_buffer_bytes_avoided": batch * P.memory_savings_bytes(
                              s["cfg"][1], s["cfg"][2], s["cfg"][6], s["cfg"][3], element_bytes=s["x"].element_size())})
 
-    # CUDA graphs instead of a tracing compiler: each layer's forward (the public API call)
-    # is captured once and replayed, so the timed loop has no Python on it. Per-layer events
-    # sit between the replays, outside the graphs.
-    graphs, launches_per_step = [], 0
+    # CUDA graphs instead of a tracing compiler: the whole step (every layer's forward, the
+    # public API call) is captured once and replayed as one graph in the timed loop, so it has
+    # no Python and one launch per step; the per-layer breakdown comes from a second loop that
+    # replays one graph per layer with events between them (outside the graphs).
+    graphs, step_graph, launches_per_step = [], None, 0
     if not args.no_graph:
         for s in state:
             g = torch.cuda.CUDAGraph()
-            c0 = _lib.launch_count()
             with torch.cuda.graph(g):
                 s["layer"].forward(s["x"], out=s["y"])
-            launches_per_step += _lib.launch_count() - c0
             graphs.append(g)
+        step_graph = torch.cuda.CUDAGraph()
+        c0 = _lib.launch_count()
+        with torch.cuda.graph(step_graph):
+            for s in state:
+                s["layer"].forward(s["x"], out=s["y"])
+        launches_per_step = _lib.launch_count() - c0
         torch.cuda.synchronize()
         for g in graphs:
             g.replay()
+        step_graph.replay()
         torch.cuda.synchronize()
 
     def step(events=None):
@@ -361,18 +367,46 @@ def run_ours(args, rank, world, local_rank):
     launches0 = _lib.launch_count()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     evs = [[torch.cuda.Event(enable_timing=True) for _ in state] for _ in range(args.steps)]
-    for k in range(args.steps):
-        if flush is not None:
-            flush.fill_(k & 0xFF)
-        starts[k].record(stream)
-        step(evs[k])
-    torch.cuda.synchronize()
-    launches = (_lib.launch_count() - launches0) + launches_per_step * args.steps
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    ms = float(np.mean([starts[k].elapsed_time(evs[k][-1]) for k in range(args.steps)]))
-    for k in range(args.steps):
+    if step_graph is not None:
+        # the timed steps (one graph replay each, between starts[k] and ends[k]) interleaved
+        # with the per-layer breakdown (per-layer graphs, events between them), so both see the
+        # same clocks and power state; only the former gives ms_per_step and value
+        # (the breakdown follows every 4th timed step: enough samples, little extra sustained load)
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        bks = list(range(0, args.steps, 4))
+        bstarts = [torch.cuda.Event(enable_timing=True) for _ in bks]
+        for k in range(args.steps):
+            if flush is not None:
+                flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+            step_graph.replay()
+            ends[k].record(stream)
+            if k % 4 == 0:
+                if flush is not None:
+                    flush.fill_((k + 1) & 0xFF)
+                bstarts[k // 4].record(stream)
+                step(evs[k // 4])
+        torch.cuda.synchronize()
+        launches = (_lib.launch_count() - launches0) + launches_per_step * args.steps  # inside the timed steps
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop()
+        ms = float(np.mean([starts[k].elapsed_time(ends[k]) for k in range(args.steps)]))
+        starts, nbreak = bstarts, len(bks)
+    else:
+        for k in range(args.steps):
+            if flush is not None:
+                flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+            step(evs[k])
+        torch.cuda.synchronize()
+        launches = _lib.launch_count() - launches0
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop()
+        ms = float(np.mean([starts[k].elapsed_time(evs[k][-1]) for k in range(args.steps)]))
+        nbreak = args.steps
+    for k in range(nbreak):
         prev = starts[k]
         for j in range(len(state)):
             per_layer[j].append(prev.elapsed_time(evs[k][j]))
@@ -497,7 +531,7 @@ def run_ours(args, rank, world, local_rank):
            "vs_baseline": None, "dtype": "bf16" if dtype == "bf16" else "f32",
            "data": "synthetic (reference splitmix64 generator, produced on device)",
            "config": {"workload": args.workload, "batch_per_gpu": batch, "layers": [s["name"] for s in state],
-                      "accumulate": "fp32", "launch": "eager" if args.no_graph else "cuda_graph_per_layer",
+                      "accumulate": "fp32", "launch": "eager" if args.no_graph else "one CUDA graph per step (per-layer graphs for the layer breakdown)",
                       "l2": (f"inputs larger than L2: {total_traffic / 1e9:.2f} GB algorithmic traffic per "
                              f"step vs 126 MB L2 (no explicit flush)" if flush is None else
                              f"L2 flushed before every step (256 MB write, untimed); {total_traffic / 1e6:.1f} MB "
