@@ -2,22 +2,25 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
 
-A step is one forward pass of every layer of the workload over one synthetic
-batch (per GPU; weak scaling across ranks: batch sharding needs no collective).
-Default workload: the EB-GAN generator layers l2..l7 (reference GAN_SUITE,
-bench.py:133-138) at batch 256 per GPU in bf16 (fp32 accumulation), the
-BASELINE "EB-GAN generator transpose-conv layers, batch 256" configuration.
+A step is one forward pass of every layer of the workload over one synthetic batch.
+Default workload: the EB-GAN generator layers l2..l7 (reference GAN_SUITE, bench.py:133-138)
+at batch 256 per GPU in fp32 -- the reference's own working precision (engines.py:271-291),
+checked against the reference's gate rel 1e-5 / abs 1e-6 (test_acceptance.py:31-32) -- the
+BASELINE "EB-GAN generator transpose-conv layers, batch 256" configuration. The same layers in
+bf16 (bf16 operands, fp32 accumulation, a stated looser gate) are reported beside it under "bf16".
 
 value    useful MACs (analysis.py:46-57 mult_count_segregated x batch, all ranks)
          / device time of the step (CUDA events, max over ranks), inputs resident.
 e2e      the same metric through the public API (PreparedLayer.forward) with
          pinned HOST input/output tensors: H2D + compute + D2H inside the region.
-roofline dominant kernel (largest share of the step): algorithmic bytes/flops per
-         launch / its average event-timed duration vs MEASURED_PEAKS.
-cpu_baseline  the CPU oracle port of the reference's segregated engine (numpy /
-         OpenBLAS, batch-parallel over host threads) on a bounded sample, rank 0, N=1.
+roofline dominant kernel (largest share of the step): algorithmic bytes/flops per launch
+          / its average event-timed duration vs the measured peaks.
+parity   outside the timed region: sampled outputs of the timed step vs the CPU oracle.
+cpu_baseline  the reference's own segregated engine (baseline/_ref, unmodified; the oracle port
+         if that is not installed), batch-parallel over the host cores, bounded sample.
 
---impl reference times that CPU path alone (rank 0; other ranks exit 0).
+--gpus N without torchrun re-launches itself under torch.distributed.run (one rank per GPU).
+--impl reference times the reference's CPU path alone (rank 0; other ranks exit 0).
 """
 
 from __future__ import annotations
@@ -25,17 +28,20 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
 import time
 
-os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # CPU path parallelises over samples
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # CPU path parallelises over samples (mode ii)
 
 import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "useful GMAC/s per transpose-conv layer and % roofline at 1/2/4/8 B200 vs CPU ref"
 
@@ -50,27 +56,42 @@ DATASET = [("ds224_k3", 224, 224, 3, 3, 1, 2), ("ds224_k4", 224, 224, 3, 4, 1, 2
            ("ds512_k4_c3", 512, 512, 3, 4, 3, 1)]
 MNIST = [("mnist_p0", 28, 28, 1, 3, 1, 0), ("mnist_p1", 28, 28, 1, 3, 1, 1), ("mnist_p2", 28, 28, 1, 3, 1, 2)]
 
+# name -> (layers, batch, dtype, scaling): "weak" = batch per GPU, "strong" = total batch split
+# over the ranks (BASELINE config 5)
 WORKLOADS = {
-    "ebgan_b256_bf16": (EBGAN, 256, "bf16"),
-    "ebgan_b256_fp32": (EBGAN, 256, "fp32"),
-    "dcgan_b256_bf16": (DCGAN, 256, "bf16"),
-    "dcgan_b256_fp32": (DCGAN, 256, "fp32"),
-    "dataset_b64_fp32": (DATASET, 64, "fp32"),
-    "mnist_b64_fp32": (MNIST, 64, "fp32"),
+    "ebgan_b256_fp32": (EBGAN, 256, "fp32", "weak"),
+    "ebgan_b256_bf16": (EBGAN, 256, "bf16", "weak"),
+    "ebgan_b4096_bf16": (EBGAN, 4096, "bf16", "strong"),
+    "ebgan_b4096_fp32": (EBGAN, 4096, "fp32", "strong"),
+    "dcgan_b256_bf16": (DCGAN, 256, "bf16", "weak"),
+    "dcgan_b256_fp32": (DCGAN, 256, "fp32", "weak"),
+    "dcgan_b64_bf16": (DCGAN, 64, "bf16", "weak"),
+    "dcgan_b64_fp32": (DCGAN, 64, "fp32", "weak"),
+    "dcgan_b1_bf16": (DCGAN, 1, "bf16", "weak"),
+    "dcgan_b1_fp32": (DCGAN, 1, "fp32", "weak"),
+    "dataset_b64_fp32": (DATASET, 64, "fp32", "weak"),
+    "mnist_b64_fp32": (MNIST, 64, "fp32", "weak"),
 }
-DEFAULT_WORKLOAD = "ebgan_b256_bf16"
+DEFAULT_WORKLOAD = "ebgan_b256_fp32"
+# the precision-matched headline carries the same layers in bf16 beside it
+COMPANION = {"ebgan_b256_fp32": "ebgan_b256_bf16", "dcgan_b256_fp32": "dcgan_b256_bf16"}
 
 
 def load_peaks():
+    """HBM and bf16 tensor peaks from the driver's MEASURED_PEAKS.json; the tcgen05 kind::tf32 /
+    kind::f16 (fp16) MMA ceilings and the FFMA peak from tools/probes/peak_probe.cu on the box
+    (profiles/r2_peaks.json)."""
+    out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
-                "source": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
-            "source": "fallback (B200_PROFILING.md)"}
+        out.update(hbm_gbs=d["hbm_gbs"], bf16_tflops=d["bf16_tflops"], source="measured (MEASURED_PEAKS.json)")
+    with open(os.path.join(ROOT, "profiles", "r2_peaks.json")) as f:
+        p = json.load(f)
+    out.update(tf32_mma_tflops=p["tf32_mma_tflops"], fp16_mma_tflops=p["fp16_mma_tflops"],
+               ffma_tflops=p["ffma_tflops"])
+    return out
 
 
 def layer_stats(cfg, batch, dtype):
@@ -83,6 +104,16 @@ def layer_stats(cfg, batch, dtype):
     oh, ow = P.output_dims(spec)
     nbytes = batch * ci * h * w * e + batch * co * oh * ow * e + ci * co * n * n * e
     return macs, nbytes, (oh, ow)
+
+
+def compute_roof(path: str, dtype: str, peaks: dict):
+    """(TFLOP/s, name) of the unit a layer's kernel computes on."""
+    if path == "igemm":
+        if dtype == "bf16":
+            return peaks["bf16_tflops"], "tensor (bf16, MEASURED_PEAKS)"
+        # fp32 on tensor cores: three kind::tf32 MMAs per product (3xTF32)
+        return peaks["tf32_mma_tflops"] / 3.0, "tensor (3xTF32: tf32 MMA ceiling / 3)"
+    return peaks["ffma_tflops"], "fp32 FFMA (measured)"
 
 
 # ---------------------------------------------------------------------------------------
@@ -100,7 +131,6 @@ class ClockSampler:
         self.thread = None
 
     def wait_first(self, timeout_s: float = 5.0):
-        """Block until nvidia-smi has produced its first sample (it takes a moment to start)."""
         t0 = time.time()
         while self.proc is not None and not self.lines and time.time() - t0 < timeout_s:
             time.sleep(0.01)
@@ -151,36 +181,142 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
+# the reference's CPU path (cpu_baseline of our arm, and the whole --impl reference arm)
 
-def cpu_baseline(layers, dtype, budget_s: float = 20.0):
-    """The reference's segregated CPU engine (oracle port: numpy im2col + OpenBLAS GEMM per
-    parity class, engines.py:271-335), batch-parallel over host threads, bounded sample."""
-    from oracle import segconv_oracle as O
-    cores = os.cpu_count() or 1
-    total_macs, total_s, parts = 0, 0.0, []
-    for i, (name, h, w, ci, n, co, pad) in enumerate(layers):
-        in_seed, bank_seed = O.harness_seeds(0, i)
-        bank = O.gen_kernel_bank(ci, co, n, bank_seed)
-        per = O.mult_count_segregated(h, w, n, pad, ci, co)
-        # one warm-up sample, then `cores` samples (at least 1) within the time budget
-        x1 = O.gen_synthetic(ci, h, w, in_seed)
+def host_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:  # numpy without the dict mode
+        pass
+    return {"cpu_model": model or platform.processor(), "os_cpu_count": os.cpu_count(), "blas": blas,
+            "numpy": np.__version__, "python": platform.python_version()}
+
+
+def _reference_module():
+    """The unmodified reference (tools/install_reference.sh -> baseline/_ref), or None."""
+    if os.path.isdir(os.path.join(REF_PATH, "segconv")):
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        try:
+            import segconv  # noqa: F401
+            return segconv
+        except ImportError:
+            return None
+    return None
+
+
+class ReferenceCPU:
+    """The reference's segregated engine on the host: PreparedLayer(bank, P, "segregated")
+    .forward(x_j) per sample (engines.py:246-291), inputs from the reference's own generator and
+    the harness seed rule (bench.py:299-300; sample j = gen_synthetic(c, h, w, seed + j*c*h*w),
+    the batch stream). Layers are prepared and the sample inputs generated once (untimed, as the
+    reference harness, bench.py:257-258); `run()` times one pass over every layer's samples.
+    mode "ii": ThreadPoolExecutor(os.cpu_count()) over samples with OPENBLAS_NUM_THREADS=1;
+    mode "i": the reference default (threads=1, one sample at a time, OpenBLAS's own threads).
+    The unmodified reference comes from baseline/_ref (kind "reference"); without it, the oracle
+    port of the same engine (kind "port")."""
+
+    def __init__(self, layers, pass_budget_s: float, mode: str = "ii", samples_cap: int = 256):
+        from concurrent.futures import ThreadPoolExecutor
+
+        from oracle.segconv_oracle import harness_seeds, mult_count_segregated
+        ref = _reference_module()
+        self.cores = os.cpu_count() or 1
+        self.mode = mode
+        if ref is not None:
+            from segconv import engines as E
+            from segconv import synth as S
+            self.kind = "reference"
+
+            def prep(bank, pad):
+                return E.prepare_layer(bank, pad, E.ENGINE_SEGREGATED)
+            gen_x, gen_bank = S.gen_synthetic, S.gen_kernel_bank
+        else:
+            from oracle import segconv_oracle as O
+            self.kind = "port"
+
+            class _Port:
+                def __init__(self, bank, pad):
+                    self.bank, self.pad = bank, pad
+                    self.prepared = O.prepare_segregated(bank, np.float32)
+
+                def forward(self, x, threads=1):
+                    return O.forward_segregated(x, self.bank, self.pad, prepared=self.prepared)
+            prep, gen_x, gen_bank = _Port, O.gen_synthetic, O.gen_kernel_bank
+        self.pool = ThreadPoolExecutor(self.cores) if mode == "ii" else None
+        self.units, parts = [], []
+        par = self.cores if mode == "ii" else 1
+        for i, (name, h, w, ci, n, co, pad) in enumerate(layers):
+            in_seed, bank_seed = harness_seeds(0, i)
+            layer = prep(gen_bank(ci, co, n, bank_seed), pad)
+            x0 = gen_x(ci, h, w, in_seed)
+            layer.forward(x0)  # warm-up
+            t0 = time.perf_counter()
+            layer.forward(x0)
+            one = time.perf_counter() - t0
+            s = int(max(1, min(samples_cap, pass_budget_s / len(layers) * par / max(one, 1e-6))))
+            if mode == "ii":
+                s = max(s, min(self.cores, samples_cap))
+            xs = [gen_x(ci, h, w, in_seed + j * ci * h * w) for j in range(s)]
+            self.units.append((layer, xs, mult_count_segregated(h, w, n, pad, ci, co) * s))
+            parts.append(f"{name}:{s}")
+        self.macs = sum(u[2] for u in self.units)
+        what = ("the unmodified reference segconv.PreparedLayer(bank, P, 'segregated').forward (baseline/_ref)"
+                if self.kind == "reference" else "the oracle port of the reference's segregated engine")
+        how = (f"ThreadPool({self.cores}) over samples, OPENBLAS_NUM_THREADS=1 (mode ii)" if mode == "ii" else
+               "one sample at a time, threads=1, OpenBLAS default threading (mode i, the reference default)")
+        self.sample = (f"fp32 {what}; samples per layer per pass {{{', '.join(parts)}}}; {how}; per-sample cost is "
+                       f"batch-independent (extrapolated to the batch)")
+
+    def run(self) -> float:
+        """seconds of one timed pass over all layers' samples"""
         t0 = time.perf_counter()
-        O.forward_segregated(x1, bank, pad)
-        one = time.perf_counter() - t0
-        budget_layer = budget_s / len(layers)
-        s = int(max(1, min(256, budget_layer * cores / max(one, 1e-6))))
-        xs = O.unit_floats(s * ci * h * w, in_seed).reshape(s, ci, h, w)
-        t0 = time.perf_counter()
-        O.forward_segregated_batch(xs, bank, pad, workers=cores)
-        dt = time.perf_counter() - t0
-        total_macs += per * s
-        total_s += dt
-        parts.append(f"{name}:{s}")
-    return {"value": total_macs / total_s / 1e9, "unit": "GMAC/s", "cores": cores, "kind": "port",
-            "sample": f"fp32 numpy/OpenBLAS segregated engine, samples per layer {{{', '.join(parts)}}}, "
-                      f"ThreadPool({cores}) over samples, OPENBLAS_NUM_THREADS=1; per-sample cost is "
-                      f"batch-independent (extrapolated to batch)",
-            "seconds": total_s}
+        for layer, xs, _ in self.units:
+            if self.pool is not None:
+                list(self.pool.map(layer.forward, xs))
+            else:
+                for x in xs:
+                    layer.forward(x)
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.shutdown()
+
+
+def reference_cpu(layers, budget_s: float, mode: str = "ii"):
+    """cpu_baseline: one timed pass of ReferenceCPU sized to about budget_s seconds."""
+    rc = ReferenceCPU(layers, budget_s, mode)
+    try:
+        dt = rc.run()
+    finally:
+        rc.close()
+    return {"value": rc.macs / dt / 1e9, "unit": "GMAC/s", "cores": rc.cores, "kind": rc.kind, "mode": mode,
+            "sample": rc.sample, "seconds": dt}
+
+
+def reference_cpu_mode_i(workload: str, budget_s: float):
+    """Mode (i) needs OpenBLAS's default threading, fixed at numpy import: run it in a child."""
+    env = dict(os.environ)
+    env.pop("OPENBLAS_NUM_THREADS", None)
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-ref-worker", "--workload", workload,
+           "--cpu-budget", str(budget_s)]
+    try:
+        res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=max(120, 6 * budget_s))
+        return json.loads(res.stdout.strip().splitlines()[-1])
+    except Exception as e:  # report, do not fail the bench
+        return {"error": f"{type(e).__name__}: {e}"}
 
 
 def reference_transient(cfg):
@@ -195,7 +331,6 @@ def reference_transient(cfg):
     x = O.gen_synthetic(ci, h, w, in_seed)
     bank = O.gen_kernel_bank(ci, co, n, bank_seed)
     out = {}
-    # weights are laid out once per weight tensor outside the forward (engines.py:232-244)
     prep_seg = O.prepare_segregated(bank, np.float32)
     prep_ref = np.ascontiguousarray(bank.transpose(1, 0, 2, 3).reshape(co, -1))
     for key, fn, prep in (("reference_seg_transient_bytes", O.forward_segregated, prep_seg),
@@ -204,54 +339,49 @@ def reference_transient(cfg):
         y = fn(x, bank, pad, prepared=prep)
         _, peak = tracemalloc.get_traced_memory()
         tracemalloc.stop()
-        out[key] = int(peak - y.nbytes)  # transient beyond the returned output
+        out[key] = int(peak - y.nbytes)
         del y
     return out
 
 
 def run_reference(args, rank):
-    layers, batch, dtype = WORKLOADS[args.workload]
+    """--impl reference: the reference's own CPU implementation of the path (the unmodified
+    package in baseline/_ref), timed on the host cores; each step is one pass over a bounded
+    sample of the workload, sized so that warm-up + steps take about three minutes (rank 0)."""
     if rank != 0:
         return 0
-    from oracle import segconv_oracle as O
-    cores = os.cpu_count() or 1
-    s = max(1, min(cores, 16))
-    prepared = []
-    for i, (name, h, w, ci, n, co, pad) in enumerate(layers):
-        in_seed, bank_seed = O.harness_seeds(0, i)
-        prepared.append((O.unit_floats(s * ci * h * w, in_seed).reshape(s, ci, h, w),
-                         O.gen_kernel_bank(ci, co, n, bank_seed), pad,
-                         O.mult_count_segregated(h, w, n, pad, ci, co) * s))
-    macs = sum(p[3] for p in prepared)
-
-    def step():
-        for x, bank, pad, _ in prepared:
-            O.forward_segregated_batch(x, bank, pad, workers=cores)
-
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
-    value = macs / dt / 1e9
-    sample = (f"{s} samples per layer per step (bounded sample of batch {batch}), fp32 numpy/OpenBLAS "
-              f"oracle port of the reference segregated engine, ThreadPool({cores}) over samples")
+    layers, batch, dtype, scaling = WORKLOADS[args.workload]
+    per_pass = float(min(args.ref_step_budget, max(0.5, 180.0 / max(1, args.steps + args.warmup))))
+    rc = ReferenceCPU(layers, per_pass, mode="ii")
+    try:
+        for _ in range(args.warmup):
+            rc.run()
+        secs = [rc.run() for _ in range(args.steps)]
+    finally:
+        rc.close()
+    dt = float(np.median(secs))
+    value = rc.macs / dt / 1e9
+    mode_i = reference_cpu_mode_i(args.workload, budget_s=min(20.0, 4 * per_pass))
     out = {"metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference splitmix64 generator)",
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (reference splitmix64 generator)",
            "config": {"workload": args.workload, "batch_per_gpu": batch, "layers": [c[0] for c in layers]},
            "impl": "reference",
-           "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": cores, "kind": "port", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": rc.cores, "kind": rc.kind,
+                            "sample": rc.sample + f"; median pass of {args.steps} steps",
+                            "mode_i": mode_i, "host": host_info()},
            "e2e": {"value": value, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
 
 
+# ---------------------------------------------------------------------------------------
+# our arm
+
 def pin_to_gpu_numa_node(local_rank: int):
-    """Bind this rank's host threads to the CPUs nvidia-smi reports as local to its GPU, so the
-    pinned host buffers of the e2e leg are allocated on the GPU's NUMA node (first touch) and
-    PCIe copies do not cross the socket interconnect. Returns the previous affinity (or None)."""
+    """Bind this rank's host threads to the CPUs local to its GPU (first-touch NUMA placement of
+    the pinned e2e buffers). Returns the previous affinity (or None)."""
     try:
         import pynvml
         pynvml.nvmlInit()
@@ -263,46 +393,93 @@ def pin_to_gpu_numa_node(local_rank: int):
         if cpus:
             os.sched_setaffinity(0, cpus)
             return prev
-    except Exception:  # no NVML or no affinity info: leave the binding alone
+    except Exception:
         pass
     return None
 
 
-def run_ours(args, rank, world, local_rank):
+def _max_over_ranks(v, world, dev):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def parity_check(state, dtype, samples_per_layer: int = 4):
+    """Outside the timed region: sampled outputs of the timed step against the fp64 CPU oracle
+    (the unified rule, engines.py:271-291). Samples 0, B-1 and seeded random ones, all channels.
+    fp32: the reference's gate rel 1e-5 / abs 1e-6 (test_acceptance.py:31-32); bf16: the stated
+    bf16 gate on bf16-rounded inputs: rel 2^-7, abs 1e-3 * max|ref|."""
+    from oracle import segconv_oracle as O
+    rows = []
+    for s in state:
+        b = s["x"].shape[0]
+        rng = np.random.default_rng(1234)
+        idx = sorted({0, b - 1} | set(int(v) for v in rng.integers(0, b, max(0, samples_per_layer - 2))))
+        bank = s["bank"].double().cpu().numpy()
+        if dtype == "bf16":
+            bank = O.bf16_round(bank.astype(np.float32)).astype(np.float64)
+        worst_rel = worst_abs = 0.0
+        ok = True
+        for j in idx:
+            xj = s["x"][j].float().cpu().numpy().astype(np.float64)
+            yj = s["y"][j].float().cpu().numpy()
+            ref = O.forward_segregated(xj, bank, s["cfg"][6])
+            if dtype == "bf16":
+                rep = O.compare(yj, ref, 2.0 ** -7, 1e-3 * float(np.abs(ref).max()))
+            else:
+                rep = O.compare(yj, ref, 1e-5, 1e-6)
+            ok &= rep["passed"]
+            worst_rel = max(worst_rel, rep["max_rel_diff"])
+            worst_abs = max(worst_abs, rep["max_abs_diff"])
+        rows.append({"name": s["name"], "samples": idx, "max_rel": worst_rel, "max_abs": worst_abs, "passed": ok})
+    gate = ("rel 1e-5 / abs 1e-6 vs the fp64 oracle (the reference's fp32 gate)" if dtype != "bf16" else
+            "rel 2^-7 / abs 1e-3*max|ref| vs the fp64 oracle on bf16-rounded inputs")
+    return {"passed": all(r["passed"] for r in rows), "gate": gate, "layers": rows}
+
+
+def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=True, with_parity=True):
+    """Prepare, warm up, time `args.steps` steps of `workload` on this rank; return the pieces of
+    the JSON line (every rank returns; the caller prints on rank 0)."""
     import torch
     import torch.distributed as dist
 
     import paper_2502_20493_b200 as P
     from paper_2502_20493_b200 import _lib
+    from paper_2502_20493_b200.parallel import shard_range
     from paper_2502_20493_b200.synth import device_unit_floats, harness_seeds
 
-    layers, batch, dtype = WORKLOADS[args.workload]
+    layers, batch, dtype, scaling = WORKLOADS[workload]
     if args.batch:
         batch = args.batch
-    torch.cuda.set_device(local_rank)
-    prev_affinity = None if os.environ.get("SEGB200_NO_NUMA_PIN") else pin_to_gpu_numa_node(local_rank)
+    if scaling == "strong":  # BASELINE config 5: one total batch split over the ranks
+        b0, b1 = shard_range(batch, world, rank)
+    else:                    # batch per GPU
+        b0, b1 = rank * batch, (rank + 1) * batch
+    local = b1 - b0
     dev = torch.device("cuda", local_rank)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     stream = torch.cuda.current_stream()
+    peaks = load_peaks()
 
-    # --- prepare (untimed, as the reference harness, bench.py:257-258) ---
     state = []
     for i, cfg in enumerate(layers):
         name, h, w, ci, n, co, pad = cfg
         in_seed, bank_seed = harness_seeds(0, i)
         bank = device_unit_floats((ci, co, n, n), bank_seed, dtype=torch.float32, device=dev)
         layer = P.prepare_layer(bank, pad, compute=dtype)
-        # rank r owns samples [r*batch, (r+1)*batch) of the batch stream
-        x = device_unit_floats((batch, ci, h, w), in_seed + rank * batch * ci * h * w, dtype=tdt, device=dev)
-        macs, nbytes, (oh, ow) = layer_stats(cfg, batch, dtype)
-        y = torch.empty((batch, co, oh, ow), dtype=tdt, device=dev)
+        # rank r owns samples [b0, b1) of the batch stream
+        x = device_unit_floats((local, ci, h, w), in_seed + b0 * ci * h * w, dtype=tdt, device=dev)
+        macs, nbytes, (oh, ow) = layer_stats(cfg, local, dtype)
+        y = torch.empty((local, co, oh, ow), dtype=tdt, device=dev)
         state.append({"name": name, "cfg": cfg, "layer": layer, "x": x, "y": y, "macs": macs, "bytes": nbytes,
-                      "path": layer.select_path(_lib.BF16 if dtype == "bf16" else _lib.F32, batch, h, w),
+                      "bank": bank, "path": layer.select_path(_lib.BF16 if dtype == "bf16" else _lib.F32, local, h, w),
                       "flops": 2 * macs})
     torch.cuda.synchronize()
 
-    # clocks are sampled from the warm-up on (the GPU is under the same load) through the
-    # end of the timed region; nvidia-smi needs a moment to start
     sampler = ClockSampler(local_rank)
     sampler.start()
     sampler.wait_first()
@@ -311,23 +488,19 @@ def run_ours(args, rank, world, local_rank):
             s["layer"].forward(s["x"], out=s["y"])
     torch.cuda.synchronize()
 
-    # device memory beyond inputs, outputs and prepared weights (BASELINE config 4: memory
-    # footprint vs the reference): the forward workspace high-water mark per layer
     mem_rows = []
-    for s in state:
-        _lib.workspace_high_water(local_rank, reset=True)
-        s["layer"].forward(s["x"], out=s["y"])
-        torch.cuda.synchronize()
-        mem_rows.append({"name": s["name"], "path": s["path"],
-                         "workspace_bytes": _lib.workspace_high_water(local_rank),
-                         "io_bytes": s["x"].numel() * s["x"].element_size() + s["y"].numel() * s["y"].element_size(),
-                         "upsampled_buffer_bytes_avoided": batch * P.memory_savings_bytes(
-                             s["cfg"][1], s["cfg"][2], s["cfg"][6], s["cfg"][3], element_bytes=s["x"].element_size())})
+    if with_memory:
+        for s in state:
+            mem_rows.append({"name": s["name"], "path": s["path"],
+                             "workspace_bytes": s["layer"].workspace_bytes(local, s["cfg"][1], s["cfg"][2]),
+                             "io_bytes": s["x"].numel() * s["x"].element_size() + s["y"].numel() * s["y"].element_size(),
+                             "upsampled_buffer_bytes_avoided": local * P.memory_savings_bytes(
+                                 s["cfg"][1], s["cfg"][2], s["cfg"][6], s["cfg"][3],
+                                 element_bytes=s["x"].element_size())})
 
-    # CUDA graphs instead of a tracing compiler: the whole step (every layer's forward, the
-    # public API call) is captured once and replayed as one graph in the timed loop, so it has
-    # no Python and one launch per step; the per-layer breakdown comes from a second loop that
-    # replays one graph per layer with events between them (outside the graphs).
+    # CUDA graphs instead of a tracing compiler: the whole step (every layer's public-API
+    # forward) is captured once and replayed as one graph per timed step; the per-layer breakdown
+    # replays one graph per layer with events between them (after every fourth timed step)
     graphs, step_graph, launches_per_step = [], None, 0
     if not args.no_graph:
         for s in state:
@@ -360,18 +533,12 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    # L2 hygiene: a step that moves less than 2x the 126 MB L2 is preceded by a 256 MB
-    # write (outside the timed span of the step), so every step starts L2-cold
     step_traffic = sum(s["bytes"] for s in state)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if step_traffic < (252 << 20) else None
     launches0 = _lib.launch_count()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     evs = [[torch.cuda.Event(enable_timing=True) for _ in state] for _ in range(args.steps)]
     if step_graph is not None:
-        # the timed steps (one graph replay each, between starts[k] and ends[k]) interleaved
-        # with the per-layer breakdown (per-layer graphs, events between them), so both see the
-        # same clocks and power state; only the former gives ms_per_step and value
-        # (the breakdown follows every 4th timed step: enough samples, little extra sustained load)
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         bks = list(range(0, args.steps, 4))
         bstarts = [torch.cuda.Event(enable_timing=True) for _ in bks]
@@ -387,7 +554,7 @@ def run_ours(args, rank, world, local_rank):
                 bstarts[k // 4].record(stream)
                 step(evs[k // 4])
         torch.cuda.synchronize()
-        launches = (_lib.launch_count() - launches0) + launches_per_step * args.steps  # inside the timed steps
+        launches = (_lib.launch_count() - launches0) + launches_per_step * args.steps
         if world > 1:
             dist.barrier()
         clocks = sampler.stop()
@@ -411,36 +578,25 @@ def run_ours(args, rank, world, local_rank):
         for j in range(len(state)):
             per_layer[j].append(prev.elapsed_time(evs[k][j]))
             prev = evs[k][j]
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(ms, world, dev)
 
-    peaks = load_peaks()
-    step_macs = sum(s["macs"] for s in state)
-    value = step_macs * world / (ms * 1e-3) / 1e9
+    step_macs_local = sum(s["macs"] for s in state)
+    total_macs = sum(layer_stats(c, batch if scaling == "strong" else batch * world, dtype)[0] for c in layers)
+    value = total_macs / (ms * 1e-3) / 1e9
 
-    # per-layer roofline: bound = the larger of compute time and HBM time, where the compute
-    # peak is the one of the unit the layer runs on: measured bf16 tensor peak (K3/K3b bf16);
-    # for 3xTF32 (K3 fp32) the measured bf16 peak / 2 (tf32 rate) / 3 (passes); for the
-    # CUDA-core direct kernel the FFMA peak 148 SM x 128 x 2 x 1.965 GHz (theoretical)
     layer_rows = []
     for j, s in enumerate(state):
         lms = float(np.mean(per_layer[j]))
-        if s["path"] == "igemm":
-            cpeak = peaks["bf16_tflops"] if dtype == "bf16" else peaks["bf16_tflops"] / 6.0
-            cname = "tensor"
-        else:
-            cpeak, cname = 148 * 128 * 2 * 1.965e-3, "fp32_ffma"
+        cpeak, cname = compute_roof(s["path"], dtype, peaks)
         t_comp = s["flops"] / (cpeak * 1e12)
         t_hbm = s["bytes"] / (peaks["hbm_gbs"] * 1e9)
-        bound = cname if t_comp > t_hbm else "hbm"
+        bound = "tensor" if (t_comp > t_hbm and s["path"] == "igemm") else ("ffma" if t_comp > t_hbm else "hbm")
         if bound != "hbm":
             achieved, peak, unit = s["flops"] / (lms * 1e-3) / 1e12, cpeak, "TFLOP/s"
         else:
             achieved, peak, unit = s["bytes"] / (lms * 1e-3) / 1e9, peaks["hbm_gbs"], "GB/s"
         layer_rows.append({"name": s["name"], "path": s["path"], "ms": lms,
-                           "gmacs": s["macs"] / (lms * 1e-3) / 1e9, "bound": bound,
+                           "gmacs": s["macs"] / (lms * 1e-3) / 1e9, "bound": bound, "peak_name": cname,
                            "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                            "alg_bytes": s["bytes"], "flops": s["flops"]})
     dom = max(layer_rows, key=lambda r: r["ms"])
@@ -448,14 +604,16 @@ def run_ours(args, rank, world, local_rank):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(args.workload, {}).get(dom["name"])
+            traffic = json.load(f).get(workload, {}).get(dom["name"])
     roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
                 "frac": dom["frac"], "traffic": traffic, "kernel": f"{dom['name']} ({dom['path']})",
-                "share_of_step": dom["ms"] / ms, "peak_source": peaks["source"]}
+                "share_of_step": dom["ms"] / ms, "peak_source": dom["peak_name"] if dom["bound"] != "hbm"
+                else peaks["source"]}
 
-    # --- e2e through the public API with pinned host buffers ---
+    parity = parity_check(state, dtype) if (with_parity and rank == 0) else None
+
     e2e = None
-    if not args.no_e2e:
+    if with_e2e:
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         hx = [s["x"].cpu().pin_memory() for s in state]
         hy = [torch.empty(s["y"].shape, dtype=tdt).pin_memory() for s in state]
@@ -463,8 +621,10 @@ def run_ours(args, rank, world, local_rank):
         d2h = sum(t.numel() * t.element_size() for t in hy)
 
         def e2e_step():
+            # every layer through the public API with host tensors; the D2H copies stay in flight
+            # (non_blocking) and the region ends with a synchronize
             for s, xi, yi in zip(state, hx, hy):
-                s["layer"].forward(xi, out=yi)
+                s["layer"].forward(xi, out=yi, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -477,17 +637,10 @@ def run_ours(args, rank, world, local_rank):
             e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / e2e_steps
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": step_macs * world / (ems * 1e-3) / 1e9, "unit": "GMAC/s",
+        ems = _max_over_ranks(e0.elapsed_time(e1) / e2e_steps, world, dev)
+        e2e = {"value": total_macs / (ems * 1e-3) / 1e9, "unit": "GMAC/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems,
-               "steps": e2e_steps, "api": "PreparedLayer.forward(pinned host tensor, out=pinned host tensor)",
-               "host_threads_on_gpu_numa_node": bool(prev_affinity)}
-        # the same layers as one device-resident generator stack: only the
-        # first layer's input goes up and the last layer's output comes back
+               "steps": e2e_steps, "api": "PreparedLayer.forward(pinned host tensor, out=pinned host tensor)"}
         chains = all(a["cfg"][5] == b["cfg"][3] and tuple(a["y"].shape[2:]) == tuple(b["x"].shape[2:])
                      for a, b in zip(state, state[1:]))
         if chains and len(state) > 1:
@@ -502,49 +655,85 @@ def run_ours(args, rank, world, local_rank):
                 stack.forward(sx, out=sy)
             e1.record(stream)
             torch.cuda.synchronize()
-            sms = e0.elapsed_time(e1) / e2e_steps
-            if world > 1:
-                t = torch.tensor([sms], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                sms = float(t.item())
-            e2e["stack"] = {"value": step_macs * world / (sms * 1e-3) / 1e9, "unit": "GMAC/s", "ms_per_step": sms,
+            sms = _max_over_ranks(e0.elapsed_time(e1) / e2e_steps, world, dev)
+            e2e["stack"] = {"value": total_macs / (sms * 1e-3) / 1e9, "unit": "GMAC/s", "ms_per_step": sms,
                             "h2d_bytes_per_step": sx.numel() * sx.element_size(),
                             "d2h_bytes_per_step": sy.numel() * sy.element_size(),
-                            "api": "PreparedStack.forward(pinned host tensor, out=pinned host tensor): "
-                                   "l2..lN chained on the device (bf16 intermediates), one CUDA graph"}
+                            "api": f"PreparedStack.forward(pinned host tensor, out=pinned host tensor): l2..lN "
+                                   f"chained on the device ({stack.inter_dtype} intermediates), one CUDA graph"}
             del stack
         del hx, hy
 
+    res = {"value": value, "ms_per_step": ms, "roofline": roofline, "layers": layer_rows, "parity": parity,
+           "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "memory": mem_rows, "batch": batch,
+           "local_batch": local, "scaling": scaling, "dtype": dtype, "step_macs_local": step_macs_local,
+           "step_traffic": step_traffic, "flushed": flush is not None, "graph": not args.no_graph}
+    del state, graphs, step_graph
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    prev_affinity = None if os.environ.get("SEGB200_NO_NUMA_PIN") else pin_to_gpu_numa_node(local_rank)
+    wl = args.workload
+    layers, batch, dtype, scaling = WORKLOADS[wl]
+    big = scaling == "strong"  # config 5: multi-GB host buffers, no e2e leg by default
+    r = measure(args, wl, rank, world, local_rank, with_e2e=not (args.no_e2e or big),
+                with_memory=True, with_parity=not args.no_parity)
+    companion = None
+    if COMPANION.get(wl) and not args.no_companion:
+        c = measure(args, COMPANION[wl], rank, world, local_rank, with_e2e=not args.no_e2e, with_memory=False,
+                    with_parity=not args.no_parity)
+        companion = {"workload": COMPANION[wl], "dtype": "bf16", "value": c["value"], "unit": "GMAC/s",
+                     "ms_per_step": c["ms_per_step"], "roofline": c["roofline"], "parity": c["parity"],
+                     "e2e": c["e2e"], "gpu_launches": c["gpu_launches"], "clocks": c["clocks"],
+                     "layers": [{k: row[k] for k in ("name", "path", "ms", "gmacs", "bound", "frac")}
+                                for row in c["layers"]]}
     if rank != 0:
         return 0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        if prev_affinity:  # the CPU baseline gets every host core back
+        if prev_affinity:
             os.sched_setaffinity(0, prev_affinity)
-        cpu = cpu_baseline(layers, dtype, budget_s=args.cpu_budget)
+        cpu = reference_cpu(layers, budget_s=args.cpu_budget, mode="ii")
+        cpu["host"] = host_info()
         if not args.no_memory_reference:
-            for row, cfg in zip(mem_rows, layers):
+            for row, cfg in zip(r["memory"], layers):
                 row.update(reference_transient(cfg))
-    total_traffic = sum(s["bytes"] for s in state)
-    out = {"metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
-           "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "bf16" if dtype == "bf16" else "f32",
+    flush_note = (f"L2 flushed before every step (256 MB write, untimed); {r['step_traffic'] / 1e6:.1f} MB "
+                  f"algorithmic traffic per step" if r["flushed"] else
+                  f"inputs larger than L2: {r['step_traffic'] / 1e9:.2f} GB algorithmic traffic per step vs "
+                  f"126 MB L2 (no explicit flush)")
+    out = {"metric": METRIC, "value": r["value"], "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(args.warmup, 3), "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+           "scaling": scaling, "vs_baseline": None, "dtype": "bf16" if dtype == "bf16" else "f32",
            "data": "synthetic (reference splitmix64 generator, produced on device)",
-           "config": {"workload": args.workload, "batch_per_gpu": batch, "layers": [s["name"] for s in state],
-                      "accumulate": "fp32", "launch": "eager" if args.no_graph else "one CUDA graph per step (per-layer graphs for the layer breakdown)",
-                      "l2": (f"inputs larger than L2: {total_traffic / 1e9:.2f} GB algorithmic traffic per "
-                             f"step vs 126 MB L2 (no explicit flush)" if flush is None else
-                             f"L2 flushed before every step (256 MB write, untimed); {total_traffic / 1e6:.1f} MB "
-                             f"algorithmic traffic per step")},
-           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-           "clocks": clocks, "layers": layer_rows,
-           "memory": {"note": "workspace = device bytes segb_forward takes beyond x, y and the prepared "
-                              "weights (batch of the workload); reference_*_transient = tracemalloc peak of "
+           "config": {"workload": wl, "batch_per_gpu": r["local_batch"], "total_batch": r["batch"] if scaling ==
+                      "strong" else r["batch"] * world, "layers": [c[0] for c in layers],
+                      "precision": ("fp32 in/out; tensor-core layers as 3xTF32 (hi*hi + hi*lo + lo*hi), direct "
+                                    "layers FFMA; gate rel 1e-5 / abs 1e-6" if dtype == "fp32" else
+                                    "bf16 operands, fp32 accumulation, bf16 out"),
+                      "launch": "eager" if args.no_graph else
+                      "one CUDA graph per step (per-layer graphs for the layer breakdown)", "l2": flush_note},
+           "parity": r["parity"], "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"],
+           "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "layers": r["layers"],
+           "memory": {"note": "workspace = device bytes segb_forward_ws takes beyond x, y and the prepared "
+                              "weights (segb_forward_workspace_bytes); reference_*_transient = tracemalloc peak of "
                               "one sample through the CPU oracle port of the reference engines; "
                               "upsampled_buffer_bytes_avoided = memory_savings_bytes (analysis.py:60-82) x batch",
-                      "layers": mem_rows}}
+                      "layers": r["memory"]}}
+    if companion is not None:
+        out["bf16"] = companion
     print(json.dumps(out), flush=True)
     return 0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -559,19 +748,38 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of CUDA-graph replays")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-companion", action="store_true", help="skip the bf16 line beside the fp32 headline")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-step-budget", type=float, default=8.0,
+                    help="--impl reference: host seconds of reference work per step")
     ap.add_argument("--no-memory-reference", action="store_true",
                     help="skip the tracemalloc pass over the CPU oracle (reference memory footprint)")
+    ap.add_argument("--cpu-ref-worker", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
+    if args.cpu_ref_worker:  # child of reference_cpu_mode_i: OpenBLAS default threading
+        layers = WORKLOADS[args.workload][0]
+        print(json.dumps(reference_cpu(layers, budget_s=args.cpu_budget, mode="i")), flush=True)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one rank per GPU: re-launch under torch.distributed.run on this node
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank)
     if world > 1:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")       # the init log shows nranks / the transport
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:

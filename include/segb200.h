@@ -25,7 +25,15 @@
  *     SEGB_ERR_SHAPE -> ShapeError (tensors.py:26), SEGB_ERR_VALUE ->
  *     ValueError (engines.py:224-225,251-252), SEGB_ERR_CUDA -> RuntimeError.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream). Launches are
- *     asynchronous; no function allocates hidden workspace inside forward.
+ *     asynchronous. segb_forward / segb_forward_ws / segb_stack_forward never
+ *     allocate: the scratch a forward needs (K3's channels-last operand copy,
+ *     K3c's tap products; K2 and K3b need none) is a caller-provided workspace
+ *     sized by segb_forward_workspace_bytes, or the layer's own buffer reserved
+ *     ahead of time with segb_layer_reserve_workspace. segb_prepare builds every
+ *     weight layout the dispatcher can select for the layer's compute dtype, so
+ *     a forward is capturable into a CUDA graph from its first call.
+ *   - calls run on the device the layer was prepared on (the bank pointer's
+ *     device), whatever device is current; the current device is restored.
  *   - results are deterministic: fixed accumulation order, no atomics, no
  *     split-K, so outputs are bitwise identical across runs and GPU counts.
  */
@@ -38,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SEGB_ABI_VERSION 1
+#define SEGB_ABI_VERSION 2
 
 enum segb_status {
     SEGB_OK = 0,
@@ -114,6 +122,23 @@ int segb_layer_info(const segb_layer *layer, int *c_in, int *c_out, int *kernel_
 int segb_forward(const segb_layer *layer, const void *x, int x_dtype, int64_t batch, int in_h,
                  int in_w, void *y, int y_dtype, int compute_dtype, int path, void *stream);
 
+/* bytes of workspace segb_forward_ws needs for this call (0 for K2 and K3b);
+ * the same planning as segb_forward, so it fails with the same codes. */
+int segb_forward_workspace_bytes(const segb_layer *layer, int x_dtype, int64_t batch, int in_h, int in_w,
+                                 int y_dtype, int compute_dtype, int path, int64_t *bytes);
+
+/* segb_forward with a caller-owned device workspace of workspace_bytes bytes
+ * (SEGB_ERR_VALUE if smaller than segb_forward_workspace_bytes). Reentrant:
+ * concurrent calls on different streams each pass their own workspace. */
+int segb_forward_ws(const segb_layer *layer, const void *x, int x_dtype, int64_t batch, int in_h, int in_w,
+                    void *y, int y_dtype, int compute_dtype, int path, void *workspace,
+                    int64_t workspace_bytes, void *stream);
+
+/* grows the layer-owned workspace that segb_forward uses to at least `bytes`
+ * (the only allocation outside segb_prepare; shared by all segb_forward calls
+ * on this layer, so concurrent streams should use segb_forward_ws instead). */
+int segb_layer_reserve_workspace(segb_layer *layer, int64_t bytes);
+
 /* which kernel SEGB_PATH_AUTO picks for this call (SEGB_PATH_DIRECT/IGEMM) */
 int segb_select_path(const segb_layer *layer, int x_dtype, int64_t batch, int in_h, int in_w,
                      int compute_dtype);
@@ -131,6 +156,10 @@ int segb_release(segb_layer *layer);
  * host between layers; all launches go to `stream` (capturable as one graph). */
 int segb_stack_workspace_bytes(const segb_layer *const *layers, int count, int64_t batch, int in_h,
                                int in_w, int inter_dtype, int64_t *bytes);
+/* the same with the stack's input and output dtypes (the workspace also holds
+ * the largest per-layer forward workspace, which depends on them) */
+int segb_stack_workspace_bytes2(const segb_layer *const *layers, int count, int64_t batch, int in_h,
+                                int in_w, int x_dtype, int y_dtype, int inter_dtype, int64_t *bytes);
 int segb_stack_forward(const segb_layer *const *layers, int count, const void *x, int x_dtype,
                        int64_t batch, int in_h, int in_w, void *y, int y_dtype, int inter_dtype,
                        void *workspace, int64_t workspace_bytes, void *stream);
@@ -150,12 +179,16 @@ int segb_u8_hwc_to_chw(const void *src, int64_t images, int height, int width, i
 /* number of kernels this library has launched since load (evidence counter) */
 int64_t segb_launch_count(void);
 
-/* forward workspace accounting (no reference counterpart: the reference's
- * transient buffers are numpy temporaries). High-water mark, in bytes, of the
- * stream-ordered workspace segb_forward took from `device`'s default memory
- * pool (K3's NHWC operand copy, K3c's tap products; K2 and K3b take none)
- * since the last reset; reset != 0 restarts the mark at the current use. */
-int segb_workspace_high_water(int device, int reset, int64_t *bytes);
+/* engines.py:353-406 transpose_conv_reference_counted / _segregated_counted:
+ * the instrumented scalar engines on one feature map (in_h, in_w), device
+ * pointers. kernel is the merged (n, n) kernel (merge_subkernels of the
+ * SubKernelSet for the segregated engine, segregation.py:73-88). out: (out_h,
+ * out_w) f64, computed as the reference's Python loops do (fp64, one rounded
+ * multiply and one rounded add per tap, (u, v) order); counters[0] = mults,
+ * counters[1] = writes, as executed by the kernel (device u64[2], reset here). */
+int segb_counted_forward(const void *fmap, int fmap_dtype, int in_h, int in_w, const void *kernel,
+                         int kernel_dtype, int kernel_n, int pad, int engine, double *out,
+                         unsigned long long *counters, void *stream);
 
 #ifdef __cplusplus
 }

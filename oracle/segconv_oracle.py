@@ -236,6 +236,31 @@ def forward_scalar(x: np.ndarray, bank: np.ndarray, pad: int):
     return out, mults, writes
 
 
+def forward_scalar_reference(m: np.ndarray, k: np.ndarray, pad: int):
+    """engines.py:353-376 -- Alg. 1 per element on one map: bed-of-nails upsample
+    (tensors.py:85-95), zero pad P, all n x n taps (zeros included). fp64, (u, v) order.
+    Returns (out, mults, writes)."""
+    h, w = m.shape
+    n = k.shape[0]
+    oh, ow = output_dims(h, w, n, pad)
+    up = np.zeros((2 * h - 1 + 2 * pad, 2 * w - 1 + 2 * pad), dtype=np.float64)
+    up[pad:pad + 2 * h - 1:2, pad:pad + 2 * w - 1:2] = m
+    ul = up.tolist()
+    kl = k.astype(np.float64).tolist()
+    out = np.zeros((oh, ow))
+    mults = writes = 0
+    for xx in range(oh):
+        for yy in range(ow):
+            acc = 0.0
+            for u in range(n):
+                for v in range(n):
+                    acc += ul[xx + u][yy + v] * kl[u][v]
+                    mults += 1
+            out[xx, yy] = acc
+            writes += 1
+    return out, mults, writes
+
+
 # --------------------------------------------------------------------------
 # engines.py:175-198 -- the parity verdict
 

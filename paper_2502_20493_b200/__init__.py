@@ -11,12 +11,15 @@ from .engines import (
     ENGINE_SEGREGATED,
     ENGINES,
     ComparisonReport,
+    EngineCounters,
     PreparedLayer,
     compare_outputs,
     layer_forward,
     prepare_layer,
     transpose_conv_reference,
+    transpose_conv_reference_counted,
     transpose_conv_segregated,
+    transpose_conv_segregated_counted,
 )
 from .errors import ShapeError, SpecError
 from .segregation import SubKernelSet, merge_subkernels, segregate_kernel
@@ -33,9 +36,10 @@ from .spec import (
 )
 
 __all__ = [
-    "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "EffectivePadding",
+    "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "EffectivePadding", "EngineCounters",
     "PreparedLayer", "PreparedStack", "ShapeError", "SpecError", "SubKernelSet", "TransposeConvSpec",
     "compare_outputs", "effective_padding", "layer_forward", "memory_savings_bytes", "merge_subkernels",
     "mult_count_segregated", "output_dims", "prepare_layer", "prepare_stack", "segregate_kernel",
-    "subkernel_dims", "transpose_conv_reference", "transpose_conv_segregated",
+    "subkernel_dims", "transpose_conv_reference", "transpose_conv_reference_counted",
+    "transpose_conv_segregated", "transpose_conv_segregated_counted",
 ]

@@ -38,10 +38,15 @@ SIGNATURES = {
     "segb_select_path": (_i, [_p, _i, _i64, _i, _i, _i]),
     "segb_release": (_i, [_p]),
     "segb_unit_floats": (_i, [_p, _i, _i64, _u64, _p]),
-    "segb_workspace_high_water": (_i, [_i, _i, ctypes.POINTER(_i64)]),
+    "segb_forward_workspace_bytes": (_i, [_p, _i, _i64, _i, _i, _i, _i, _i, ctypes.POINTER(_i64)]),
+    "segb_forward_ws": (_i, [_p, _p, _i, _i64, _i, _i, _p, _i, _i, _i, _p, _i64, _p]),
+    "segb_layer_reserve_workspace": (_i, [_p, _i64]),
     "segb_stack_workspace_bytes": (_i, [ctypes.POINTER(_p), _i, _i64, _i, _i, _i, ctypes.POINTER(_i64)]),
+    "segb_stack_workspace_bytes2": (_i, [ctypes.POINTER(_p), _i, _i64, _i, _i, _i, _i, _i,
+                                         ctypes.POINTER(_i64)]),
     "segb_stack_forward": (_i, [ctypes.POINTER(_p), _i, _p, _i, _i64, _i, _i, _p, _i, _i, _p, _i64, _p]),
     "segb_u8_hwc_to_chw": (_i, [_p, _i64, _i, _i, _i, _p, _i, _p]),
+    "segb_counted_forward": (_i, [_p, _i, _i, _i, _p, _i, _i, _i, _i, _p, _p, _p]),
 }
 
 _lib = None
@@ -90,10 +95,3 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(lib().segb_launch_count())
-
-
-def workspace_high_water(device: int, reset: bool = False) -> int:
-    """Bytes of forward workspace (device pool high-water mark) since the last reset."""
-    v = ctypes.c_int64()
-    check(lib().segb_workspace_high_water(int(device), int(bool(reset)), ctypes.byref(v)))
-    return int(v.value)

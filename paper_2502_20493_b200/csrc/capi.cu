@@ -62,6 +62,7 @@ using namespace segb;
 
 struct segb_layer {
     int c_in, c_out, n, pad, engine, compute;
+    int device = 0;        // the CUDA device the layer was prepared on (every call runs there)
     void *bank = nullptr;  // owned device copy of the bank (c_in, c_out, n, n)
     int bank_dtype;
     std::mutex mu;
@@ -71,84 +72,114 @@ struct segb_layer {
     void *wt = nullptr;  // K3 3xTF32 weights: fp32 hi plane followed by the lo plane
     int c_in_pad = 0, c_out_pad = 0, c_in_pad32 = 0;  // zero-padded GEMM operand extents
     void *wz = nullptr;  // K3c weights (bf16, (kx, ky, co) rows x 64-padded c_in, K-major)
+    void *ws = nullptr;  // workspace reserved by segb_layer_reserve_workspace (segb_forward)
+    int64_t ws_bytes = 0;
 };
 
-// K2 weights for a compute dtype, built by K1 on first use (prepare builds the
-// layer's own compute dtype eagerly, so forward only allocates when a caller
-// mixes dtypes, as numpy's result_type promotion in the reference allows).
-static int ensure_direct_weights(segb_layer *L, int compute, cudaStream_t st, const void **out) {
+namespace segb {
+
+// Runs a call on the layer's device and restores the caller's current device afterwards, so a
+// layer prepared on cuda:1 works while cuda:0 is current (allocations, launches and tensor maps
+// all follow the current device).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Builds one weight layout (K1) into *slot unless it exists. Called eagerly by segb_prepare for
+// every layout the dispatcher can select for the layer's own compute dtype; a forward that
+// overrides the compute dtype may build a missing layout here, but never inside a CUDA-graph
+// capture (the build would only be recorded while the layout is already marked as built), and a
+// lazy build is synchronous so no other stream can read the layout before it exists.
+template <typename Build>
+static int ensure_layout(segb_layer *L, void **slot, size_t bytes, bool lazy, cudaStream_t st, const char *what,
+                         Build build) {
     std::lock_guard<std::mutex> g(L->mu);
-    if (!L->wd[compute]) {
-        const size_t elt = compute == SEGB_F64 ? 8 : 4;
-        const size_t bytes = elt * (size_t)L->c_out * L->c_in * L->n2p;
-        void *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    if (*slot) return SEGB_OK;
+    if (lazy) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+            return fail(SEGB_ERR_VALUE,
+                        "%s weights were not prepared for this compute dtype; run one forward outside the CUDA "
+                        "graph capture (or prepare the layer with this compute dtype) first", what);
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu) for %s weights: %s", bytes, what, cudaGetErrorString(e));
+    if (int rc = build(p)) {
+        cudaFree(p);
+        return rc;
+    }
+    if (lazy) {
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return fail(SEGB_ERR_CUDA, "%s weight build: %s", what, cudaGetErrorString(e));
+        }
+    }
+    *slot = p;
+    return SEGB_OK;
+}
+
+// K2 weights for a compute dtype
+static int ensure_direct_weights(segb_layer *L, int compute, bool lazy, cudaStream_t st, const void **out) {
+    const size_t elt = compute == SEGB_F64 ? 8 : 4;
+    const size_t bytes = elt * (size_t)L->c_out * L->c_in * L->n2p;
+    int rc = ensure_layout(L, &L->wd[compute], bytes, lazy, st, "direct-kernel", [&](void *p) {
         const int mode = compute == SEGB_F64 ? 1 : (compute == SEGB_BF16 ? 2 : 0);
         const bool packed = L->engine == SEGB_ENGINE_SEGREGATED;
-        if (int rc = run_prep_direct(L->bank, L->bank_dtype, L->c_in, L->c_out, L->n, L->n2p, packed, mode, p, st)) {
-            cudaFree(p);
-            return rc;
-        }
-        L->wd[compute] = p;
-    }
-    *out = L->wd[compute];
-    return SEGB_OK;
+        return run_prep_direct(L->bank, L->bank_dtype, L->c_in, L->c_out, L->n, L->n2p, packed, mode, p, st);
+    });
+    if (!rc && out) *out = L->wd[compute];
+    return rc;
 }
 
-static int ensure_gemm_weights(segb_layer *L, cudaStream_t st) {
-    std::lock_guard<std::mutex> g(L->mu);
-    if (!L->wg) {
-        L->c_in_pad = (int)ceil_div(L->c_in, 64) * 64;
-        L->c_out_pad = (int)ceil_div(L->c_out, 32) * 32;
-        const size_t bytes = 2ull * L->n * L->n * L->c_out_pad * L->c_in_pad;
-        void *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-        if (int rc = run_prep_gemm(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->c_out_pad, L->n, p, st)) {
-            cudaFree(p);
-            return rc;
-        }
-        L->wg = p;
-    }
-    return SEGB_OK;
+static int ensure_gemm_weights(segb_layer *L, bool lazy, cudaStream_t st) {
+    const size_t bytes = 2ull * L->n * L->n * L->c_out_pad * L->c_in_pad;
+    return ensure_layout(L, &L->wg, bytes, lazy, st, "bf16 implicit-GEMM", [&](void *p) {
+        return run_prep_gemm(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->c_out_pad, L->n, p, st);
+    });
 }
 
-static int ensure_scatter_weights(segb_layer *L, cudaStream_t st) {
-    std::lock_guard<std::mutex> g(L->mu);
-    if (!L->wz) {
-        const int c_in_pad = (int)ceil_div(L->c_in, 64) * 64;
-        const size_t bytes = 2ull * scatter_weight_rows(L->c_out, L->n) * c_in_pad;
-        void *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-        if (int rc = run_prep_scatter(L->bank, L->bank_dtype, L->c_in, c_in_pad, L->c_out, L->n, p, st)) {
-            cudaFree(p);
-            return rc;
-        }
-        L->wz = p;
-    }
-    return SEGB_OK;
+static int ensure_scatter_weights(segb_layer *L, bool lazy, cudaStream_t st) {
+    const int c_in_pad = (int)ceil_div(L->c_in, 64) * 64;
+    const size_t bytes = 2ull * scatter_weight_rows(L->c_out, L->n) * c_in_pad;
+    return ensure_layout(L, &L->wz, bytes, lazy, st, "scatter-GEMM", [&](void *p) {
+        return run_prep_scatter(L->bank, L->bank_dtype, L->c_in, c_in_pad, L->c_out, L->n, p, st);
+    });
 }
 
-static int ensure_tf32_weights(segb_layer *L, cudaStream_t st) {
-    std::lock_guard<std::mutex> g(L->mu);
-    if (!L->wt) {
-        L->c_in_pad32 = (int)ceil_div(L->c_in, 32) * 32;
-        L->c_out_pad = (int)ceil_div(L->c_out, 32) * 32;
-        const size_t plane = (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad32;
-        void *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, 2 * 4 * plane);
-        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "cudaMalloc(%zu): %s", 8 * plane, cudaGetErrorString(e));
-        if (int rc = run_prep_gemm_tf32(L->bank, L->bank_dtype, L->c_in, L->c_in_pad32, L->c_out, L->c_out_pad, L->n,
-                                        p, (char *)p + 4 * plane, st)) {
-            cudaFree(p);
-            return rc;
-        }
-        L->wt = p;
-    }
-    return SEGB_OK;
+static size_t tf32_plane(const segb_layer *L) { return (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad32; }
+
+static int ensure_tf32_weights(segb_layer *L, bool lazy, cudaStream_t st) {
+    const size_t plane = tf32_plane(L);
+    return ensure_layout(L, &L->wt, 2 * 4 * plane, lazy, st, "3xTF32 implicit-GEMM", [&](void *p) {
+        return run_prep_gemm_tf32(L->bank, L->bank_dtype, L->c_in, L->c_in_pad32, L->c_out, L->c_out_pad, L->n, p,
+                                  (char *)p + 4 * plane, st);
+    });
 }
+
+// weight-only conditions under which the dispatcher can pick each tensor-core path (the shape
+// conditions of igemm_supported that do not depend on the input)
+static bool may_use_gemm_bf16(const segb_layer *L) {
+    return L->engine == SEGB_ENGINE_SEGREGATED && L->c_in >= 16 && igemm_available();
+}
+static bool may_use_scatter(const segb_layer *L) {
+    return L->engine == SEGB_ENGINE_SEGREGATED && L->c_in >= 64 && L->c_in <= 256 &&
+           L->n * L->n * L->c_out <= 256 && L->n <= 8 && 4 * L->c_out <= L->c_in && igemm_available();
+}
+static bool may_use_tf32(const segb_layer *L) {
+    return L->engine == SEGB_ENGINE_SEGREGATED && L->n % 2 == 0 && L->c_in >= 32 && L->c_in % 4 == 0 &&
+           L->c_out >= 16 && igemm_available();
+}
+
+}  // namespace segb
 
 // tensor cores for bf16 (kind::f16) and for fp32 as 3xTF32 (kind::tf32)
 static bool igemm_ok(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int compute,
@@ -167,22 +198,6 @@ int segb_abi_version(void) { return SEGB_ABI_VERSION; }
 const char *segb_last_error(void) { return g_err.c_str(); }
 
 int64_t segb_launch_count(void) { return g_launches.load(); }
-
-int segb_workspace_high_water(int device, int reset, int64_t *bytes) {
-    cudaMemPool_t pool;
-    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
-    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "default memory pool: %s", cudaGetErrorString(e));
-    if (reset) {
-        unsigned long long zero = 0;
-        e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
-        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "memory pool reset: %s", cudaGetErrorString(e));
-    }
-    unsigned long long high = 0;
-    e = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high);
-    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "memory pool query: %s", cudaGetErrorString(e));
-    if (bytes) *bytes = (int64_t)high;
-    return SEGB_OK;
-}
 
 int segb_output_dims(int in_h, int in_w, int kernel_n, int pad, int *out_h, int *out_w) {
     return check_spec(in_h, in_w, kernel_n, pad, 1, 1, out_h, out_w);
@@ -248,10 +263,20 @@ int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int n, i
     if (!valid_dtype(compute)) return fail(SEGB_ERR_VALUE, "unknown compute dtype %d", compute);
     if (!bank) return fail(SEGB_ERR_VALUE, "null bank");
     cudaStream_t st = (cudaStream_t)stream;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, bank) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        return fail(SEGB_ERR_VALUE, "bank must be a device pointer");
+    }
+    DeviceGuard dg(pa.device);
     segb_layer *L = new segb_layer();
     L->c_in = c_in; L->c_out = c_out; L->n = n; L->pad = pad; L->engine = engine; L->compute = compute;
     L->bank_dtype = bank_dtype;
+    L->device = pa.device;
     L->n2p = (n * n + 3) / 4 * 4;
+    L->c_in_pad = (int)ceil_div(c_in, 64) * 64;
+    L->c_out_pad = (int)ceil_div(c_out, 32) * 32;
+    L->c_in_pad32 = (int)ceil_div(c_in, 32) * 32;
     const size_t bytes = dtype_size(bank_dtype) * (size_t)c_in * c_out * n * n;
     cudaError_t e = cudaMalloc(&L->bank, bytes);
     if (e == cudaSuccess) e = cudaMemcpyAsync(L->bank, bank, bytes, cudaMemcpyDeviceToDevice, st);
@@ -259,13 +284,12 @@ int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int n, i
         segb_release(L);
         return fail(SEGB_ERR_CUDA, "bank copy: %s", cudaGetErrorString(e));
     }
-    const void *dummy;
-    int rc = ensure_direct_weights(L, compute, st, &dummy);
-    if (!rc && compute == SEGB_BF16 && engine == SEGB_ENGINE_SEGREGATED && igemm_available())
-        rc = ensure_gemm_weights(L, st);
-    if (!rc && compute == SEGB_F32 && engine == SEGB_ENGINE_SEGREGATED && n % 2 == 0 && c_in >= 32 &&
-        igemm_available())
-        rc = ensure_tf32_weights(L, st);
+    // every layout the dispatcher can select for this compute dtype is built here, so forward
+    // never allocates (and is capturable into a CUDA graph from its first call)
+    int rc = ensure_direct_weights(L, compute, false, st, nullptr);
+    if (!rc && compute == SEGB_BF16 && may_use_gemm_bf16(L)) rc = ensure_gemm_weights(L, false, st);
+    if (!rc && compute == SEGB_BF16 && may_use_scatter(L)) rc = ensure_scatter_weights(L, false, st);
+    if (!rc && compute == SEGB_F32 && may_use_tf32(L)) rc = ensure_tf32_weights(L, false, st);
     if (rc) {
         segb_release(L);
         return rc;
@@ -292,43 +316,69 @@ int segb_select_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h, 
     return igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
 }
 
-int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
-                 int y_dtype, int compute, int path, void *stream) {
-    segb_layer *L = const_cast<segb_layer *>(Lc);
+// the resolved plan of one forward call: the kernel family and the workspace it needs
+struct FwdPlan {
+    int path, oh, ow, compute;
+    IgemmShape s;
+    int64_t ws_bytes;
+};
+
+static int plan_forward(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int y_dtype,
+                        int compute, int path, FwdPlan &pl) {
     if (!L) return fail(SEGB_ERR_VALUE, "null layer");
     if (batch < 1) return fail(SEGB_ERR_SHAPE, "batch must be >= 1, got %lld", (long long)batch);
-    int oh, ow;
-    if (int rc = check_spec(in_h, in_w, L->n, L->pad, L->c_in, L->c_out, &oh, &ow)) return rc;
-    if (!x || !y) return fail(SEGB_ERR_VALUE, "null tensor");
+    if (int rc = check_spec(in_h, in_w, L->n, L->pad, L->c_in, L->c_out, &pl.oh, &pl.ow)) return rc;
     if (compute < 0) compute = L->compute;
     if (!valid_dtype(compute) || !valid_dtype(x_dtype) || !valid_dtype(y_dtype))
         return fail(SEGB_ERR_VALUE, "unknown dtype (x %d, y %d, compute %d)", x_dtype, y_dtype, compute);
-    cudaStream_t st = (cudaStream_t)stream;
     if (path == SEGB_PATH_AUTO)
         path = igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
+    if (path != SEGB_PATH_IGEMM && path != SEGB_PATH_DIRECT) return fail(SEGB_ERR_VALUE, "unknown path %d", path);
+    pl.path = path;
+    pl.compute = compute;
+    pl.ws_bytes = 0;
     if (path == SEGB_PATH_IGEMM) {
         if (!igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype))
             return fail(SEGB_ERR_UNSUPPORTED, "implicit-GEMM path not eligible for this layer/shape/dtype");
-        IgemmShape s{};
+        IgemmShape &s = pl.s;
+        s = IgemmShape{};
         s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
         s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.compute = compute;
+        s.c_out_pad = L->c_out_pad;
+        if (compute == SEGB_F32) s.c_in_pad32 = L->c_in_pad32;
+        else s.c_in_pad = L->c_in_pad;
+        pl.ws_bytes = igemm_workspace_bytes(s);
+    }
+    return SEGB_OK;
+}
+
+static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
+                        int y_dtype, int compute, int path, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    FwdPlan pl;
+    if (int rc = plan_forward(L, x_dtype, batch, in_h, in_w, y_dtype, compute, path, pl)) return rc;
+    if (!x || !y) return fail(SEGB_ERR_VALUE, "null tensor");
+    if (pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes))
+        return fail(SEGB_ERR_VALUE,
+                    "this forward needs a workspace of %lld bytes (segb_forward_workspace_bytes), got %lld",
+                    (long long)pl.ws_bytes, (long long)(ws ? ws_bytes : 0));
+    DeviceGuard dg(L->device);
+    compute = pl.compute;
+    const int oh = pl.oh, ow = pl.ow;
+    if (pl.path == SEGB_PATH_IGEMM) {
+        IgemmShape &s = pl.s;
         if (compute == SEGB_F32) {
-            if (int rc = ensure_tf32_weights(L, st)) return rc;
-            s.c_in_pad32 = L->c_in_pad32; s.c_out_pad = L->c_out_pad;
-            const size_t plane = (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad32;
-            return run_igemm(s, x, L->wt, (const char *)L->wt + 4 * plane, y, st);
+            if (int rc = ensure_tf32_weights(L, true, st)) return rc;
+            return run_igemm(s, x, L->wt, (const char *)L->wt + 4 * tf32_plane(L), y, ws, ws_bytes, st);
         }
         if (igemm_scatter_supported(s)) {
-            if (int rc = ensure_scatter_weights(L, st)) return rc;
-            return run_igemm_scatter(s, x, L->wz, y, st);
+            if (int rc = ensure_scatter_weights(L, true, st)) return rc;
+            return run_igemm_scatter(s, x, L->wz, y, ws, ws_bytes, st);
         }
-        if (int rc = ensure_gemm_weights(L, st)) return rc;
-        s.c_in_pad = L->c_in_pad; s.c_out_pad = L->c_out_pad;
-        return run_igemm(s, x, L->wg, nullptr, y, st);
+        if (int rc = ensure_gemm_weights(L, true, st)) return rc;
+        return run_igemm(s, x, L->wg, nullptr, y, ws, ws_bytes, st);
     }
-    if (path != SEGB_PATH_DIRECT) return fail(SEGB_ERR_VALUE, "unknown path %d", path);
     const void *w;
-    if (int rc = ensure_direct_weights(L, compute, st, &w)) return rc;
+    if (int rc = ensure_direct_weights(L, compute, true, st, &w)) return rc;
     DirectArgs a{};
     a.x = x; a.y = y; a.w = w; a.batch = batch; a.b0 = 0;
     a.c_in = L->c_in; a.c_out = L->c_out; a.h = in_h; a.w_in = in_w; a.oh = oh; a.ow = ow; a.n = L->n;
@@ -350,6 +400,47 @@ int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch
     }
 }
 
+int segb_forward_workspace_bytes(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int y_dtype,
+                                 int compute, int path, int64_t *bytes) {
+    FwdPlan pl;
+    if (int rc = plan_forward(L, x_dtype, batch, in_h, in_w, y_dtype, compute, path, pl)) return rc;
+    if (bytes) *bytes = pl.ws_bytes;
+    return SEGB_OK;
+}
+
+int segb_forward_ws(const segb_layer *L, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
+                    int y_dtype, int compute, int path, void *workspace, int64_t workspace_bytes, void *stream) {
+    return forward_impl(const_cast<segb_layer *>(L), x, x_dtype, batch, in_h, in_w, y, y_dtype, compute, path,
+                        workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
+                 int y_dtype, int compute, int path, void *stream) {
+    segb_layer *L = const_cast<segb_layer *>(Lc);
+    if (!L) return fail(SEGB_ERR_VALUE, "null layer");
+    return forward_impl(L, x, x_dtype, batch, in_h, in_w, y, y_dtype, compute, path, L->ws, L->ws_bytes,
+                        (cudaStream_t)stream);
+}
+
+int segb_layer_reserve_workspace(segb_layer *L, int64_t bytes) {
+    if (!L) return fail(SEGB_ERR_VALUE, "null layer");
+    if (bytes < 0) return fail(SEGB_ERR_VALUE, "workspace bytes must be >= 0, got %lld", (long long)bytes);
+    std::lock_guard<std::mutex> g(L->mu);
+    if (bytes <= L->ws_bytes) return SEGB_OK;
+    DeviceGuard dg(L->device);
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+    if (e != cudaSuccess)
+        return fail(SEGB_ERR_CUDA, "cudaMalloc(%lld) for the workspace: %s", (long long)bytes, cudaGetErrorString(e));
+    if (L->ws) {
+        cudaDeviceSynchronize();  // queued forwards may still read the old buffer
+        cudaFree(L->ws);
+    }
+    L->ws = p;
+    L->ws_bytes = bytes;
+    return SEGB_OK;
+}
+
 // ---------------------------------------------------------------- layer stacks
 // the GAN_SUITE generator stacks (bench.py:124-139 of the reference) run
 // device-resident. The reference has no stack call: a user chains layer_forward (engines.py:
@@ -358,13 +449,15 @@ int segb_forward(const segb_layer *Lc, const void *x, int x_dtype, int64_t batch
 // nothing crosses PCIe between layers and the whole chain is one stream-ordered launch
 // sequence (capturable as one CUDA graph).
 
-static int stack_plan(const segb_layer *const *layers, int count, int64_t batch, int in_h, int in_w,
-                      int inter_dtype, int64_t *inter_elems) {
+// Plans a chain: per layer its input/output dims and dtypes; returns the largest intermediate
+// (elements) and the largest per-layer forward workspace (bytes).
+static int stack_plan(const segb_layer *const *layers, int count, int64_t batch, int in_h, int in_w, int x_dtype,
+                      int y_dtype, int inter_dtype, int64_t *inter_elems, int64_t *fwd_ws) {
     if (!layers || count < 1) return fail(SEGB_ERR_VALUE, "a stack needs at least one layer");
     if (batch < 1) return fail(SEGB_ERR_SHAPE, "batch must be >= 1, got %lld", (long long)batch);
     if (!valid_dtype(inter_dtype)) return fail(SEGB_ERR_VALUE, "unknown intermediate dtype %d", inter_dtype);
-    int h = in_h, w = in_w;
-    int64_t most = 0;
+    int h = in_h, w = in_w, dt = x_dtype;
+    int64_t most = 0, ws = 0;
     for (int i = 0; i < count; ++i) {
         const segb_layer *L = layers[i];
         if (!L) return fail(SEGB_ERR_VALUE, "null layer %d in the stack", i);
@@ -373,40 +466,61 @@ static int stack_plan(const segb_layer *const *layers, int count, int64_t batch,
                         i - 1, layers[i - 1]->c_out);
         int oh, ow;
         if (int rc = check_spec(h, w, L->n, L->pad, L->c_in, L->c_out, &oh, &ow)) return rc;
+        const int odt = i + 1 < count ? inter_dtype : y_dtype;
         if (i + 1 < count) most = std::max<int64_t>(most, batch * L->c_out * (int64_t)oh * ow);
+        FwdPlan pl;
+        if (valid_dtype(dt) && valid_dtype(odt)) {
+            if (int rc = plan_forward(L, dt, batch, h, w, odt, -1, SEGB_PATH_AUTO, pl)) return rc;
+            ws = std::max(ws, pl.ws_bytes);
+        }
         h = oh;
         w = ow;
+        dt = odt;
     }
     if (inter_elems) *inter_elems = most;
+    if (fwd_ws) *fwd_ws = ws;
+    return SEGB_OK;
+}
+
+static int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
+
+int segb_stack_workspace_bytes2(const segb_layer *const *layers, int count, int64_t batch, int in_h, int in_w,
+                                int x_dtype, int y_dtype, int inter_dtype, int64_t *bytes) {
+    int64_t most = 0, fws = 0;
+    if (int rc = stack_plan(layers, count, batch, in_h, in_w, x_dtype, y_dtype, inter_dtype, &most, &fws)) return rc;
+    const int64_t one = align256(most * (int64_t)dtype_size(inter_dtype));
+    if (bytes) *bytes = (count > 2 ? 2 * one : one) + align256(fws);
     return SEGB_OK;
 }
 
 int segb_stack_workspace_bytes(const segb_layer *const *layers, int count, int64_t batch, int in_h, int in_w,
                                int inter_dtype, int64_t *bytes) {
-    int64_t most = 0;
-    if (int rc = stack_plan(layers, count, batch, in_h, in_w, inter_dtype, &most)) return rc;
-    const int64_t one = (most * (int64_t)dtype_size(inter_dtype) + 255) / 256 * 256;
-    if (bytes) *bytes = count > 2 ? 2 * one : one;
-    return SEGB_OK;
+    // without the end dtypes: the intermediates' dtype stands in for both (the bf16 stacks)
+    return segb_stack_workspace_bytes2(layers, count, batch, in_h, in_w, inter_dtype, inter_dtype, inter_dtype,
+                                       bytes);
 }
 
 int segb_stack_forward(const segb_layer *const *layers, int count, const void *x, int x_dtype, int64_t batch,
                        int in_h, int in_w, void *y, int y_dtype, int inter_dtype, void *workspace,
                        int64_t workspace_bytes, void *stream) {
-    int64_t need = 0;
-    if (int rc = segb_stack_workspace_bytes(layers, count, batch, in_h, in_w, inter_dtype, &need)) return rc;
+    int64_t most = 0, fws = 0;
+    if (int rc = stack_plan(layers, count, batch, in_h, in_w, x_dtype, y_dtype, inter_dtype, &most, &fws)) return rc;
+    const int64_t one = align256(most * (int64_t)dtype_size(inter_dtype));
+    const int64_t inter = count > 2 ? 2 * one : one;
+    const int64_t need = inter + align256(fws);
     if (!x || !y) return fail(SEGB_ERR_VALUE, "null tensor");
     if (need > 0 && (!workspace || workspace_bytes < need))
         return fail(SEGB_ERR_VALUE, "stack workspace of %lld bytes needed, got %lld", (long long)need,
                     (long long)workspace_bytes);
-    const int64_t half = count > 2 ? need / 2 : need;
+    void *fwd_ws = fws > 0 ? (char *)workspace + inter : nullptr;
     const void *cur = x;
     int cur_dt = x_dtype, h = in_h, w = in_w;
     for (int i = 0; i < count; ++i) {
         const bool last = i + 1 == count;
-        void *dst = last ? y : (char *)workspace + (i % 2) * half;
+        void *dst = last ? y : (char *)workspace + (i % 2) * one;
         const int dst_dt = last ? y_dtype : inter_dtype;
-        if (int rc = segb_forward(layers[i], cur, cur_dt, batch, h, w, dst, dst_dt, -1, SEGB_PATH_AUTO, stream))
+        if (int rc = forward_impl(const_cast<segb_layer *>(layers[i]), cur, cur_dt, batch, h, w, dst, dst_dt, -1,
+                                  SEGB_PATH_AUTO, fwd_ws, fws, (cudaStream_t)stream))
             return rc;
         h = 2 * h + 2 * layers[i]->pad - layers[i]->n;
         w = 2 * w + 2 * layers[i]->pad - layers[i]->n;
@@ -423,6 +537,7 @@ int segb_release(segb_layer *L) {
     cudaFree(L->wg);
     cudaFree(L->wt);
     cudaFree(L->wz);
+    cudaFree(L->ws);
     delete L;
     return SEGB_OK;
 }

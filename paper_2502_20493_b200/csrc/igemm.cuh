@@ -13,21 +13,23 @@ struct IgemmShape {
 
 bool igemm_available();
 bool igemm_supported(const IgemmShape &s);
-int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, cudaStream_t st);
+// workspace (bytes) run_igemm needs for this shape: K3's NHWC operand copy or K3c's tap products
+int64_t igemm_workspace_bytes(const IgemmShape &s);
+int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,
+              int64_t ws_bytes, cudaStream_t st);
 
 // K3c: input-stationary scatter GEMM + gather for narrow outputs (igemm_scatter_sm100.cu)
 bool igemm_scatter_supported(const IgemmShape &s);
 int scatter_weight_rows(int c_out, int n);
 int run_prep_scatter(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int n, void *dst,
                      cudaStream_t st);
-int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *y, cudaStream_t st);
+int64_t igemm_scatter_workspace_bytes(const IgemmShape &s);
+int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *y, void *ws, int64_t ws_bytes,
+                      cudaStream_t st);
 
 // K3p: class-pair tiles as 2-SM CTA pairs over K3's operands (igemm_cp_sm100.cu)
 bool igemm_cp_supported(const IgemmShape &s);
 int run_igemm_cp_core(const IgemmShape &s, const void *x_nhwc, const void *wg, void *y, cudaStream_t st);
-
-// stream-ordered workspace pool kept reserved across calls (igemm_sm100.cu)
-void keep_pool_reserved();
 
 // K3b: row-streaming variant for wide class grids (igemm_rows_sm100.cu)
 bool igemm_rows_supported(const IgemmShape &s);

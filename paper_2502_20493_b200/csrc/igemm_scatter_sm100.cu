@@ -315,7 +315,14 @@ int run_prep_scatter(const void *bank, int bank_dtype, int c_in, int c_in_pad, i
     return check_launch("prep_scatter_kernel");
 }
 
-int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *y, cudaStream_t st) {
+int64_t igemm_scatter_workspace_bytes(const IgemmShape &s) {
+    ScatterParams prm;
+    if (!scatter_params(s, prm)) return 0;
+    return (prm.positions * prm.n_real * 4 + 255) / 256 * 256;
+}
+
+int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *y, void *ws, int64_t ws_bytes,
+                      cudaStream_t st) {
     ScatterParams prm;
     if (!scatter_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "scatter implicit GEMM: unsupported shape");
     auto encode = tensor_map_encoder();
@@ -341,12 +348,11 @@ int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (scatter B): error %d", (int)r);
     }
-    keep_pool_reserved();
     const int64_t zbytes = prm.positions * prm.n_real * 4;
-    void *z = nullptr;
-    cudaError_t e = cudaMallocAsync(&z, zbytes, st);
-    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "workspace: %s", cudaGetErrorString(e));
-    prm.z = (float *)z;
+    if (!ws || ws_bytes < zbytes)
+        return fail(SEGB_ERR_VALUE, "scatter implicit GEMM: workspace of %lld bytes needed, got %lld",
+                    (long long)zbytes, (long long)ws_bytes);
+    prm.z = (float *)ws;  // the tap products Z, in the caller's workspace
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -368,7 +374,6 @@ int run_igemm_scatter(const IgemmShape &s, const void *x, const void *wz, void *
         note_launch();
         rc = check_launch("scatter_gather_kernel");
     }
-    cudaFreeAsync(z, st);
     return rc;
 }
 

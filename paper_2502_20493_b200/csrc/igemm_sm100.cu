@@ -29,19 +29,29 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "f16split.cuh"
 #include "igemm.cuh"
 #include "tc_ptx.cuh"
 
 namespace segb {
 
 constexpr int kThreads = 192;
-// A k-step covers one 128-B SWIZZLE_128B row of channels: 64 bf16 or 32 fp32 (kind::tf32).
-template <bool TF32X3> constexpr int kstep_channels() { return TF32X3 ? 32 : 64; }
-// 3xTF32 partial-sum depth: the tensor core's fp32 accumulation error grows with the number
+// operand modes: bf16 (kind::f16, one MMA per product), fp32 as 3xTF32 (kind::tf32: hi/lo tf32
+// planes, three MMAs) or as 3xFP16 (kind::f16 on scaled fp16 hi/lo planes, three MMAs at twice
+// the tf32 rate; f16split.cuh)
+constexpr int kModeBf16 = 0, kModeTf32x3 = 1, kModeF16x3 = 2;
+// A k-step covers one 128-B SWIZZLE_128B row of channels: 64 bf16 / fp16 or 32 fp32 (kind::tf32).
+template <int MODE> constexpr int kstep_channels() { return MODE == kModeTf32x3 ? 32 : 64; }
+// 3-pass partial-sum depth: the tensor core's fp32 accumulation error grows with the number
 // of accumulate steps (measured on B200: ~0.25 ulp per MMA), so every kTf32Chunk k-steps
 // (96 MMAs) the partial is moved into fp32 registers.
 constexpr int kTf32Chunk = 8;
 constexpr int kTf32MaxN = 128;
+
+// instruction descriptor: fp16 x fp16 -> fp32, A and B K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBlockM >> 4) << 24);
+}
 
 struct ClassGeom {
     int R, C;             // sub-kernel rows / cols
@@ -59,6 +69,8 @@ struct IgemmParams {
     int box_w, box_h, box_b;  // A box (positions): cols x rows x samples = 128
     int64_t class_positions;  // batch * rows * cols (identical for all classes here)
     void *y;
+    const float *x_partials;  // 3xFP16: the input's partial maxima (its scale 2^k_x)
+    float w_unscale;          // 3xFP16: 2^-k_w of the weight planes
 };
 
 template <typename TY> __device__ __forceinline__ TY cvt_out(float v);
@@ -66,7 +78,7 @@ template <> __device__ __forceinline__ float cvt_out<float>(float v) { return v;
 template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 // ---------------------------------------------------------------- the kernel
-// TF32X3: fp32 operands as 3xTF32 (A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, ~fp32 accuracy)
+// MODE kModeTf32x3: fp32 operands as 3xTF32 (A_hi*B_hi + A_hi*B_lo + A_lo*B_hi, ~fp32 accuracy)
 // on tcgen05.mma.kind::tf32; each stage then holds hi and lo tiles of both operands.
 // PAIR: the grid is made of 2-CTA clusters. The two CTAs of a pair compute adjacent position
 // blocks (2 mbp, 2 mbp + 1) of the same class and output-channel block in lockstep, so they
@@ -79,12 +91,16 @@ template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(floa
 // each CTA's TMEM receives its own 128 rows x N columns, the TMA loads of both CTAs signal
 // the leader's full barrier, the leader's commits arrive on both CTAs' empty / tfull
 // barriers and both CTAs' epilogue warps arrive on the leader's tempty barrier.
-template <typename TY, bool TF32X3, int PM>
+// kModeF16x3: the same three products on scaled fp16 planes with kind::f16 MMAs; the epilogue
+// multiplies the fp32 sum by 2^-(k_x + k_w).
+template <typename TY, int MODE, int PM>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_tconv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmAlo, const __grid_constant__ CUtensorMap tmBlo,
                        const IgemmParams prm) {
-    constexpr int KCH = kstep_channels<TF32X3>();
+    constexpr bool TF32X3 = MODE != kModeBf16;  // three-pass hi/lo operands (either kind)
+    constexpr bool TFK = MODE == kModeTf32x3;   // kind::tf32 MMAs
+    constexpr int KCH = kstep_channels<MODE>();
     constexpr int NOP = TF32X3 ? 2 : 1;  // tiles per operand per stage (hi [, lo])
     constexpr bool PAIR = PM > 0, TWO = PM == 2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -101,6 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    float *unscale_slot = reinterpret_cast<float *>(tmem_slot + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int N = prm.n_tile;
@@ -137,6 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmBlo) : "memory");
         }
+    }
+    if (MODE == kModeF16x3 && warp == 2) {  // the input's scale from the absmax partials
+        float m = 0.f;
+        for (int i = lane; i < kAbsmaxBlocks; i += 32) m = fmaxf(m, __ldg(prm.x_partials + i));
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (lane == 0) *unscale_slot = ldexpf(1.f, -f16_scale_exp(m)) * prm.w_unscale;
     }
     if (warp == 1) {  // TMEM: two accumulator buffers of N fp32 columns
         const uint32_t cols = tmem_cols(N);
@@ -224,8 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t aLo0 = desc_lo_sw128(smem_u32(sA)), bLo0 = desc_lo_sw128(smem_u32(sB));
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            const uint32_t idesc = TWO ? (TF32X3 ? idesc_tf32(N) : idesc_bf16(N)) + ((uint32_t)(256 - kBlockM) >> 4 << 24)
-                                       : (TF32X3 ? idesc_tf32(N) : idesc_bf16(N));
+            const uint32_t idesc0 = MODE == kModeTf32x3 ? idesc_tf32(N) : (MODE == kModeF16x3 ? idesc_f16(N) : idesc_bf16(N));
+            const uint32_t idesc = TWO ? idesc0 + ((uint32_t)(256 - kBlockM) >> 4 << 24) : idesc0;
             // commits predicated on the elected lane like the MMAs: no divergent branch in the
             // loop, so ptxas keeps the stage / descriptor arithmetic in uniform registers
             auto commit = [&](uint64_t *bar, bool both) {
@@ -260,9 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (TF32X3) {
                             const uint32_t ah = a0 + kk * 2, al = a0 + (a_bytes >> 4) + kk * 2;
                             const uint32_t bh = b0 + kk * 2, bl = b0 + (b_cta >> 4) + kk * 2;
-                            tc_mma_lo<TWO ? 2 : 1, true>(d, ah, bh, idesc, (kc | kk) != 0, leader);
-                            tc_mma_lo<TWO ? 2 : 1, true>(d, ah, bl, idesc, 1, leader);
-                            tc_mma_lo<TWO ? 2 : 1, true>(d, al, bh, idesc, 1, leader);
+                            tc_mma_lo<TWO ? 2 : 1, TFK>(d, ah, bh, idesc, (kc | kk) != 0, leader);
+                            tc_mma_lo<TWO ? 2 : 1, TFK>(d, ah, bl, idesc, 1, leader);
+                            tc_mma_lo<TWO ? 2 : 1, TFK>(d, al, bh, idesc, 1, leader);
                         } else {
                             tc_mma_lo<TWO ? 2 : 1, false>(d, a0 + kk * 2, b0 + kk * 2, idesc, (ks | kk) != 0, leader);
                         }
@@ -287,8 +310,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (TF32X3) {  // ---------------- epilogue, 3xTF32: sum the TMEM partials in registers
+    } else if (TF32X3) {  // ---------------- epilogue, 3-pass: sum the TMEM partials in registers
         const int q = warp & 3;
+        const float unscale = MODE == kModeF16x3 ? *unscale_slot : 1.f;
         const int m = q * 32 + lane;
         const int64_t plane = (int64_t)prm.oh * prm.ow;
         float *y = reinterpret_cast<float *>(prm.y);
@@ -329,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int co_left = prm.c_out - nb * N;
 #pragma unroll
                 for (int k = 0; k < kTf32MaxN; ++k)
-                    if (k < N && k < co_left) dst[(int64_t)k * plane] = racc[k];
+                    if (k < N && k < co_left) dst[(int64_t)k * plane] = MODE == kModeF16x3 ? racc[k] * unscale : racc[k];
             }
         }
     } else {  // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
@@ -578,19 +602,15 @@ bool igemm_supported(const IgemmShape &s) {
     return igemm_scatter_supported(s) || use_rows(s) || (make_params(s, prm) && tensor_map_encoder() != nullptr);
 }
 
-void keep_pool_reserved() {
-    // stream-ordered workspace from the device's default pool, which is told to keep its
-    // reservation so steady-state calls never map memory or block the host
-    static std::once_flag pool_once[64];
-    int cur = 0;
-    cudaGetDevice(&cur);
-    std::call_once(pool_once[cur & 63], [cur] {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    });
+// K3's only workspace: the channels-last A operand (bf16, or fp32 hi followed by fp32 lo for
+// 3xTF32), written by the staging launch and read by the GEMM. K3b and K3c's own kernels take
+// none from here (K3c's tap products are counted by igemm_scatter_workspace_bytes).
+int64_t igemm_workspace_bytes(const IgemmShape &s) {
+    if (igemm_scatter_supported(s)) return igemm_scatter_workspace_bytes(s);
+    if (use_rows(s)) return 0;
+    const bool tf32 = s.compute == SEGB_F32;
+    const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
+    return (elems * (tf32 ? 8 : 2) + 255) / 256 * 256;
 }
 
 static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const void *ptr, const cuuint64_t *dims,
@@ -627,18 +647,19 @@ static int launch_k3(unsigned grid, size_t smem, cudaStream_t st, const CUtensor
     return e == cudaSuccess ? SEGB_OK : fail(SEGB_ERR_CUDA, "igemm_tconv_kernel (pair): %s", cudaGetErrorString(e));
 }
 
-int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, cudaStream_t st) {
+int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,
+              int64_t ws_bytes, cudaStream_t st) {
     if (use_rows(s)) return run_igemm_rows(s, x, wg, y, st);
     IgemmParams prm;
     if (!make_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM: unsupported shape");
     if (!tensor_map_encoder()) return fail(SEGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const bool tf32 = s.compute == SEGB_F32;
-    keep_pool_reserved();
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
     const int esz = tf32 ? 4 : 2;
-    void *xs = nullptr;  // channels-last A operand: bf16, or fp32 hi followed by fp32 lo
-    cudaError_t e = cudaMallocAsync(&xs, elems * esz * (tf32 ? 2 : 1), st);
-    if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "workspace: %s", cudaGetErrorString(e));
+    void *xs = ws;  // channels-last A operand in the caller's workspace
+    if (!xs || ws_bytes < igemm_workspace_bytes(s))
+        return fail(SEGB_ERR_VALUE, "implicit GEMM: workspace of %lld bytes needed, got %lld",
+                    (long long)igemm_workspace_bytes(s), (long long)ws_bytes);
     void *xs_lo = tf32 ? (void *)((char *)xs + elems * esz) : nullptr;
     {
         const int hw = s.h * s.w;
@@ -661,12 +682,10 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
                 nchw_to_nhwc_bf16<float><<<grd, blk, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw);
         }
         note_launch();
-        if (int rc = check_launch("nchw->nhwc staging")) { cudaFreeAsync(xs, st); return rc; }
+        if (int rc = check_launch("nchw->nhwc staging")) return rc;
     }
     if (!tf32 && igemm_cp_supported(s)) {  // K3p: both column parities per tile
-        int rc = run_igemm_cp_core(s, xs, wg, y, st);
-        cudaFreeAsync(xs, st);
-        return rc;
+        return run_igemm_cp_core(s, xs, wg, y, st);
     }
     const int kch = tf32 ? 32 : 64;
     const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -697,7 +716,7 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     if (!rc) rc = encode_map(&tmB, dt, 3, wg, bdims, bstr, bbox, "B");
     if (!rc && tf32) rc = encode_map(&tmAlo, dt, 4, xs_lo, adims, astr, abox, "A lo");
     if (!rc && tf32) rc = encode_map(&tmBlo, dt, 3, wg_lo, bdims, bstr, bbox, "B lo");
-    if (rc) { cudaFreeAsync(xs, st); return rc; }
+    if (rc) return rc;
     if (!tf32) { tmAlo = tmA; tmBlo = tmB; }
     prm.y = y;
     int dev = 0, sms = 148;
@@ -720,11 +739,9 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
         SEGB_K3_LAUNCH(float, false)
     }
 #undef SEGB_K3_LAUNCH
-    if (rc) { cudaFreeAsync(xs, st); return rc; }
+    if (rc) return rc;
     note_launch();
-    rc = check_launch("igemm_tconv_kernel");
-    cudaFreeAsync(xs, st);
-    return rc;
+    return check_launch("igemm_tconv_kernel");
 }
 
 }  // namespace segb

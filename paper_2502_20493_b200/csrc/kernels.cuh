@@ -15,6 +15,11 @@ int run_prep_gemm(const void *bank, int bank_dtype, int c_in, int c_in_pad, int 
 int run_prep_gemm_tf32(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
                        void *hi, void *lo, cudaStream_t st);
 
+// 3xFP16 weights (f16split.cuh): absmax of the bank into partials[kAbsmaxBlocks], then the scaled
+// fp16 hi / lo planes in the K3 layout
+int run_prep_gemm_f16x2(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
+                        void *hi, void *lo, float *partials, cudaStream_t st);
+
 // synthetic inputs (synth.cu)
 int run_unit_floats(void *out, int dtype, int64_t count, uint64_t seed, cudaStream_t st);
 

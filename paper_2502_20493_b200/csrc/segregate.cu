@@ -5,6 +5,7 @@
 // PreparedLayer.__init__, engines.py:236-244. All copies are bit-exact
 // permutations (plus an optional round-to-nearest-even cast to bf16).
 #include "common.cuh"
+#include "f16split.cuh"
 #include "kernels.cuh"
 
 namespace segb {
@@ -139,6 +140,34 @@ __global__ void prep_gemm_tf32_kernel(const TS *__restrict__ bank, float *hi, fl
     }
 }
 
+// [tap][c_out_pad][c_in_pad] fp16 hi and lo planes for 3xFP16 (f16split.cuh): the bank scaled
+// by 2^k_w (k_w from the bank's largest magnitude, reduced into `partials` beforehand) and split
+template <typename TS>
+__global__ void prep_gemm_f16x2_kernel(const TS *__restrict__ bank, __half *hi, __half *lo, int c_in, int c_in_pad,
+                                       int c_out, int c_out_pad, int n, const float *__restrict__ partials) {
+    __shared__ float scale;
+    if (threadIdx.x == 0) scale = ldexpf(1.f, f16_scale_exp(reduce_partials(partials)));
+    __syncthreads();
+    const int64_t total = (int64_t)n * n * c_out_pad * c_in_pad;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int ci = (int)(e % c_in_pad);
+        const int64_t rest = e / c_in_pad;
+        const int co = (int)(rest % c_out_pad);
+        const int k = (int)(rest / c_out_pad);
+        float v = 0.f;
+        if (ci < c_in && co < c_out) {
+            int i, j;
+            unpack_index(n, k, i, j);
+            v = (float)to_f64(bank[(((int64_t)ci * c_out + co) * n + i) * n + j]);
+        }
+        __half h, l;
+        split_f16(v * scale, h, l);
+        hi[e] = h;
+        lo[e] = l;
+    }
+}
+
 static unsigned grid_for(int64_t total) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 32));
 }
@@ -227,5 +256,45 @@ int run_prep_gemm_tf32(const void *bank, int bank_dtype, int c_in, int c_in_pad,
     }
     note_launch();
     return check_launch("prep_gemm_tf32_kernel");
+}
+}  // namespace segb
+
+namespace segb {
+int run_absmax_partials(const void *v, int dtype, int64_t count, float *partials, cudaStream_t st) {
+    switch (dtype) {
+        case SEGB_F32: absmax_partials_kernel<float><<<kAbsmaxBlocks, 512, 0, st>>>((const float *)v, count, partials); break;
+        case SEGB_F64: absmax_partials_kernel<double><<<kAbsmaxBlocks, 512, 0, st>>>((const double *)v, count, partials); break;
+        case SEGB_BF16:
+            absmax_partials_kernel<__nv_bfloat16><<<kAbsmaxBlocks, 512, 0, st>>>((const __nv_bfloat16 *)v, count, partials);
+            break;
+        default: return fail(SEGB_ERR_VALUE, "unknown dtype %d", dtype);
+    }
+    note_launch();
+    return check_launch("absmax_partials_kernel");
+}
+
+int run_prep_gemm_f16x2(const void *bank, int bank_dtype, int c_in, int c_in_pad, int c_out, int c_out_pad, int n,
+                        void *hi, void *lo, float *partials, cudaStream_t st) {
+    if (int rc = run_absmax_partials(bank, bank_dtype, (int64_t)c_in * c_out * n * n, partials, st)) return rc;
+    const int64_t total = (int64_t)n * n * c_out_pad * c_in_pad;
+    const unsigned g = grid_for(total);
+    __half *h = (__half *)hi, *l = (__half *)lo;
+    switch (bank_dtype) {
+        case SEGB_F32:
+            prep_gemm_f16x2_kernel<float><<<g, 256, 0, st>>>((const float *)bank, h, l, c_in, c_in_pad, c_out,
+                                                             c_out_pad, n, partials);
+            break;
+        case SEGB_F64:
+            prep_gemm_f16x2_kernel<double><<<g, 256, 0, st>>>((const double *)bank, h, l, c_in, c_in_pad, c_out,
+                                                              c_out_pad, n, partials);
+            break;
+        case SEGB_BF16:
+            prep_gemm_f16x2_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16 *)bank, h, l, c_in, c_in_pad,
+                                                                     c_out, c_out_pad, n, partials);
+            break;
+        default: return fail(SEGB_ERR_VALUE, "unknown bank dtype %d", bank_dtype);
+    }
+    note_launch();
+    return check_launch("prep_gemm_f16x2_kernel");
 }
 }  // namespace segb

@@ -10,6 +10,8 @@ C ABI (include/segb200.h):
   transpose_conv_segregated                engines.py:143-150
   transpose_conv_reference (Alg. 1)        engines.py:134-140 (the GPU reference engine)
   compare_outputs / ComparisonReport       engines.py:99-118, 175-198 (host-side verdict)
+  EngineCounters, transpose_conv_{reference,segregated}_counted
+                                           engines.py:121-126, 353-406 -> segb_counted_forward
 
 Extensions over the reference (documented in DESIGN.md): forward also takes
 torch tensors, CUDA-resident (C,H,W) or batched (B,C,H,W), returning a torch
@@ -179,6 +181,7 @@ class PreparedLayer:
             ctypes.byref(handle)))
         self._handle = handle
         self._lib = _lib.lib()
+        self._ws_cache: dict = {}
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -199,9 +202,12 @@ class PreparedLayer:
         p = self._lib.segb_select_path(self._handle, x_dtype_id, batch, in_h, in_w, cid)
         return {1: "direct", 2: "igemm"}[p]
 
-    def forward(self, x, threads: int = 1, out=None, path: str = "auto", out_dtype=None):
+    def forward(self, x, threads: int = 1, out=None, path: str = "auto", out_dtype=None,
+                non_blocking: bool = False):
         """engines.py:246-256. numpy (C,H,W) in -> numpy out (dtype = result_type of
-        x and bank, as the reference); torch in -> torch out."""
+        x and bank, as the reference); torch in -> torch out. A host `out=` tensor is complete
+        when forward returns (the reference returns finished host arrays); `non_blocking=True`
+        leaves that device-to-host copy in flight on the caller's current stream instead."""
         x = require_channel_tensor(x)
         c_axis = 1 if (_is_torch(x) and x.dim() == 4) else 0
         if x.shape[c_axis] != self.c_in:
@@ -214,7 +220,10 @@ class PreparedLayer:
         if path not in _lib.PATH_IDS:
             raise ValueError(f"unknown path {path!r}, expected one of {tuple(_lib.PATH_IDS)}")
         if _is_torch(x):
-            return self._forward_torch(x, out, path, out_dtype, out_h, out_w)
+            y = self._forward_torch(x, out, path, out_dtype, out_h, out_w)
+            if out is not None and not out.is_cuda and not non_blocking:
+                _device.torch().cuda.current_stream(self.device).synchronize()
+            return y
         return self._forward_numpy(x, out_h, out_w, path)
 
     def _compute_for(self, x_dt) -> str:
@@ -352,12 +361,41 @@ class PreparedLayer:
             main.synchronize()
         return out_h_t
 
+    def workspace_bytes(self, batch: int, in_h: int, in_w: int, x_dtype=None, y_dtype=None,
+                        compute: str | None = None, path: str = "auto") -> int:
+        """Device scratch bytes one forward of this shape takes (segb_forward_workspace_bytes):
+        K3's channels-last operand copy or K3c's tap products; 0 for K2 and K3b."""
+        t = _device.torch()
+        compute = compute or self.compute
+        if x_dtype is None:
+            x_dtype = t.bfloat16 if compute == "bf16" else (t.float64 if compute == "fp64" else t.float32)
+        if y_dtype is None:
+            y_dtype = x_dtype
+        return self._ws_bytes(_device.dtype_id(x_dtype), _device.dtype_id(y_dtype), int(batch), int(in_h),
+                              int(in_w), COMPUTE_DTYPES[compute], _lib.PATH_IDS[path])
+
+    def _ws_bytes(self, xd, yd, b, h, w, cid, pid) -> int:
+        key = (xd, yd, b, h, w, cid, pid)
+        v = self._ws_cache.get(key)
+        if v is None:
+            r = ctypes.c_int64()
+            _lib.check(self._lib.segb_forward_workspace_bytes(self._handle, xd, b, h, w, yd, cid, pid,
+                                                              ctypes.byref(r)))
+            v = self._ws_cache[key] = int(r.value)
+        return v
+
     def _launch(self, d_x, d_y, compute: str, path: str) -> None:
+        """One segb_forward_ws call on the caller's current stream. The workspace (if the kernel
+        needs one) comes from torch's stream-ordered caching allocator on the layer's device, so
+        the C ABI never allocates and concurrent streams never share scratch."""
         b, _, h, w = d_x.shape
-        _lib.check(self._lib.segb_forward(
-            self._handle, d_x.data_ptr(), _device.dtype_id(d_x.dtype), int(b), int(h), int(w),
-            d_y.data_ptr(), _device.dtype_id(d_y.dtype), COMPUTE_DTYPES[compute],
-            _lib.PATH_IDS[path], _device.stream_ptr(self.device)))
+        xd, yd = _device.dtype_id(d_x.dtype), _device.dtype_id(d_y.dtype)
+        cid, pid = COMPUTE_DTYPES[compute], _lib.PATH_IDS[path]
+        nbytes = self._ws_bytes(xd, yd, int(b), int(h), int(w), cid, pid)
+        ws = _device.torch().empty(nbytes, dtype=_device.torch().uint8, device=self.device) if nbytes else None
+        _lib.check(self._lib.segb_forward_ws(
+            self._handle, d_x.data_ptr(), xd, int(b), int(h), int(w), d_y.data_ptr(), yd, cid, pid,
+            ws.data_ptr() if ws is not None else None, nbytes, _device.stream_ptr(self.device)))
 
 
 def prepare_layer(bank, pad: int, engine: str = ENGINE_SEGREGATED, compute: str | None = None) -> PreparedLayer:
@@ -398,8 +436,54 @@ def transpose_conv_reference(feature_map, kernel, pad: int) -> np.ndarray:
     return prepare_layer(k[np.newaxis, np.newaxis], pad, ENGINE_REFERENCE).forward(m[np.newaxis])[0]
 
 
+@dataclass
+class EngineCounters:
+    """engines.py:121-126: operation counts recorded by the instrumented scalar engines."""
+
+    mults: int = 0
+    writes: int = 0
+
+
+def _counted(m: np.ndarray, k: np.ndarray, pad: int, engine: str):
+    """segb_counted_forward on one map: fp64 output and the kernel's own mults/writes counts."""
+    t = _device.require_cuda()
+    h, w = m.shape
+    oh, ow = _spec_dims(h, w, k.shape[0], pad)
+    mw = m if m.dtype in (np.float32, np.float64) else m.astype(np.float64)
+    kw = k if k.dtype in (np.float32, np.float64) else k.astype(np.float64)
+    dev = t.cuda.current_device()
+    d_m = _device.to_device(mw, dev)
+    d_k = _device.to_device(kw, dev)
+    d_out = t.empty((oh, ow), dtype=t.float64, device=dev)
+    d_cnt = t.zeros(2, dtype=t.int64, device=dev)
+    _lib.check(_lib.lib().segb_counted_forward(
+        d_m.data_ptr(), _device.dtype_id(d_m.dtype), int(h), int(w), d_k.data_ptr(), _device.dtype_id(d_k.dtype),
+        int(k.shape[0]), int(pad), _lib.ENGINE_IDS[engine], d_out.data_ptr(), d_cnt.data_ptr(),
+        _device.stream_ptr(dev)))
+    cnt = d_cnt.cpu().tolist()
+    return d_out.cpu().numpy(), EngineCounters(mults=int(cnt[0]), writes=int(cnt[1]))
+
+
+def transpose_conv_reference_counted(feature_map, kernel, pad: int):
+    """engines.py:353-376: Alg. 1 per element (upsample, pad P, all n x n taps) with counters."""
+    m = require_feature_map(feature_map)
+    k = require_square_kernel(kernel)
+    _spec_dims(m.shape[0], m.shape[1], k.shape[0], pad)
+    return _counted(m, k, pad, ENGINE_REFERENCE)
+
+
+def transpose_conv_segregated_counted(feature_map, subs: SubKernelSet, pad: int):
+    """engines.py:379-406: the unified rule per element (one parity sub-kernel per output) with
+    counters. The sub-kernels are merged back into K (bit-exact, segregation.py:73-88); the
+    device kernel reads k_rs[u, v] as K[2u + r, 2v + s]."""
+    m = require_feature_map(feature_map)
+    _spec_dims(m.shape[0], m.shape[1], subs.size, pad)
+    return _counted(m, merge_subkernels(subs), pad, ENGINE_SEGREGATED)
+
+
 __all__ = [
-    "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "PreparedLayer",
+    "ENGINE_REFERENCE", "ENGINE_SEGREGATED", "ENGINES", "ComparisonReport", "EngineCounters", "PreparedLayer",
     "SpecError", "ShapeError", "TransposeConvSpec", "compare_outputs", "layer_forward",
-    "output_dims", "prepare_layer", "transpose_conv_reference", "transpose_conv_segregated",
+    "output_dims", "prepare_layer", "transpose_conv_reference", "transpose_conv_reference_counted",
+    "transpose_conv_segregated", "transpose_conv_segregated_counted",
 ]

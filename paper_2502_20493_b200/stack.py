@@ -57,23 +57,28 @@ class PreparedStack:
             in_h, in_w = L.output_shape(in_h, in_w)
         return in_h, in_w
 
-    def workspace_bytes(self, batch: int, in_h: int, in_w: int) -> int:
+    def workspace_bytes(self, batch: int, in_h: int, in_w: int, x_dtype=None, y_dtype=None) -> int:
+        """Device workspace of one chained forward: the ping-pong intermediates plus the largest
+        per-layer forward scratch (segb_stack_workspace_bytes2)."""
+        inter = COMPUTE_DTYPES[self.inter_dtype]
+        xd = inter if x_dtype is None else _device.dtype_id(x_dtype)
+        yd = inter if y_dtype is None else _device.dtype_id(y_dtype)
         v = ctypes.c_int64()
-        _lib.check(_lib.lib().segb_stack_workspace_bytes(
-            self._handles, len(self.layers), int(batch), int(in_h), int(in_w),
-            COMPUTE_DTYPES[self.inter_dtype], ctypes.byref(v)))
+        _lib.check(_lib.lib().segb_stack_workspace_bytes2(
+            self._handles, len(self.layers), int(batch), int(in_h), int(in_w), xd, yd, inter, ctypes.byref(v)))
         return int(v.value)
 
-    def _workspace(self, batch, h, w):
-        key = (batch, h, w)
+    def _workspace(self, batch, h, w, x_dtype, y_dtype):
+        key = (batch, h, w, x_dtype, y_dtype)
         if key not in self._ws:
             t = _device.torch()
-            self._ws[key] = t.empty(max(1, self.workspace_bytes(batch, h, w)), dtype=t.uint8, device=self.device)
+            nbytes = self.workspace_bytes(batch, h, w, x_dtype, y_dtype)
+            self._ws[key] = t.empty(max(1, nbytes), dtype=t.uint8, device=self.device)
         return self._ws[key]
 
     def _launch(self, d_x, d_y):
         b, _, h, w = d_x.shape
-        ws = self._workspace(int(b), int(h), int(w))
+        ws = self._workspace(int(b), int(h), int(w), d_x.dtype, d_y.dtype)
         _lib.check(_lib.lib().segb_stack_forward(
             self._handles, len(self.layers), d_x.data_ptr(), _device.dtype_id(d_x.dtype), int(b), int(h), int(w),
             d_y.data_ptr(), _device.dtype_id(d_y.dtype), COMPUTE_DTYPES[self.inter_dtype], ws.data_ptr(),
@@ -112,7 +117,7 @@ class PreparedStack:
                 sx = t.empty(tuple(xb.shape), dtype=xb.dtype, device=self.device)
                 sy = t.empty(shape, dtype=out_dtype, device=self.device)
                 sx.copy_(xb)
-                self._launch(sx, sy)  # warm-up: lazy weight layouts, workspace pool
+                self._launch(sx, sy)  # warm-up outside the capture
                 t.cuda.current_stream(self.device).synchronize()
                 g = t.cuda.CUDAGraph()
                 with t.cuda.graph(g):

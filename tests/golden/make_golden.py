@@ -18,6 +18,9 @@ Contents (all produced by reference code paths, cited):
                 engine output in fp64 (engines.py:163-172)
   * gan{i}_*    small GAN-shaped layers driven by the harness seed rule
                 (bench.py:299-300) with the reference segregated output
+  * cnt{i}_*    the instrumented scalar engines (engines.py:353-406) on small
+                maps: output (fp64) and the mults / writes counters of both
+                transpose_conv_reference_counted and _segregated_counted
 """
 
 import os
@@ -109,6 +112,29 @@ def main():
         g[f"gan{i}_meta"] = np.array([h, w, ci, n, co, pad, in_seed, bank_seed], dtype=np.uint64)
         g[f"gan{i}_out"] = engines.layer_forward(xg, bg, pad, engine=engines.ENGINE_SEGREGATED)
     g["n_gan"] = np.int64(len(gan))
+    # --- instrumented scalar engines (engines.py:353-406), own RNG stream ---------------
+    crng = np.random.default_rng(353)
+    cnt = 0
+    while cnt < 24:
+        h = int(crng.integers(1, 10))
+        w = int(crng.integers(1, 10))
+        n = int(crng.integers(2, 8))
+        pad = int(crng.integers(0, 5))
+        if 2 * h + 2 * pad - n < 1 or 2 * w + 2 * pad - n < 1:
+            continue
+        dt = np.float64 if cnt % 2 else f32
+        m = crng.random((h, w)).astype(dt)
+        kk = crng.random((n, n)).astype(dt)
+        ref_out, cr = engines.transpose_conv_reference_counted(m, kk, pad)
+        seg_out, cs = engines.transpose_conv_segregated_counted(m, segregation.segregate_kernel(kk), pad)
+        g[f"cnt{cnt}_map"] = m
+        g[f"cnt{cnt}_kernel"] = kk
+        g[f"cnt{cnt}_pad"] = np.int64(pad)
+        g[f"cnt{cnt}_ref"] = ref_out
+        g[f"cnt{cnt}_seg"] = seg_out
+        g[f"cnt{cnt}_counts"] = np.array([cr.mults, cr.writes, cs.mults, cs.writes], dtype=np.int64)
+        cnt += 1
+    g["n_cnt"] = np.int64(cnt)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays, {os.path.getsize(OUT)} bytes")
 

@@ -1,0 +1,86 @@
+"""Multi-process sharding with the real CUDA kernels (VERDICT r1 "Weak 8").
+
+gpurun and the round-end runs give one GPU, so the two ranks share cuda:0 (their kernels are
+independent launches -- nothing waits on another rank inside a kernel) and exchange their output
+shards over gloo on host copies. What is checked is the sharding itself: batch shards and
+output-channel shards of an l6/l7-shaped layer, run through PreparedLayer on each rank,
+gathered, equal the single-process output -- bit for bit for batch shards (SURVEY 8(e):
+per-sample arithmetic is unchanged by the partition), within the dtype's rounding for channel
+shards (a channel slice can select another kernel variant).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+# (c_in, c_out, n, pad, batch, h, w, compute): ebgan_l6 / l7 shapes at a small batch, and an
+# fp32 (3xTF32) GAN layer
+CASES = [(128, 64, 4, 2, 6, 64, 64, "bf16"), (64, 64, 4, 2, 5, 128, 128, "bf16"), (256, 128, 4, 2, 4, 16, 16, "fp32")]
+
+
+def _worker(rank, world, port, case, mode, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_20493_b200 as P
+    from oracle import segconv_oracle as O
+    from paper_2502_20493_b200.parallel import gather_batch, gather_channels, prepare_channel_shard, shard_batch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        ci, co, n, pad, b, h, w, compute = case
+        tdt = torch.bfloat16 if compute == "bf16" else torch.float32
+        bank = O.gen_kernel_bank(ci, co, n, 17)
+        x = device_unit_floats((b, ci, h, w), 23, dtype=tdt)
+        if mode == "batch":
+            layer = P.prepare_layer(bank, pad, compute=compute)
+            y = layer.forward(shard_batch(x, world, rank).contiguous())
+            full = gather_batch(y.cpu(), b)  # gloo: host copies of the shards
+        else:
+            layer, _ = prepare_channel_shard(bank, pad, world, rank, compute=compute)
+            full = gather_channels(layer.forward(x).cpu(), co)
+        torch.save(full, os.path.join(out_dir, f"rank{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["batch", "channel"])
+@pytest.mark.parametrize("case", CASES, ids=["l6_bf16", "l7_bf16", "gan_fp32"])
+def test_two_ranks_bitwise_equal_one(tmp_path, case, mode):
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2502_20493_b200 as P
+    from oracle import segconv_oracle as O
+    from paper_2502_20493_b200.synth import device_unit_floats
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    mp.start_processes(_worker, args=(2, _free_port(), case, mode, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    ci, co, n, pad, b, h, w, compute = case
+    tdt = torch.bfloat16 if compute == "bf16" else torch.float32
+    one = P.prepare_layer(O.gen_kernel_bank(ci, co, n, 17), pad, compute=compute).forward(
+        device_unit_floats((b, ci, h, w), 23, dtype=tdt)).cpu()
+    for r in range(2):
+        got = torch.load(tmp_path / f"rank{r}.pt")
+        if mode == "batch":  # the same kernel over the same samples: bitwise
+            assert torch.equal(got, one), (r, mode)
+        else:  # a channel slice may dispatch to another kernel variant (its own summation order)
+            rel = 2.0 ** -7 if compute == "bf16" else 1e-5
+            rep = O.compare(got.float().numpy(), one.float().numpy(), rel, 1e-6)
+            assert rep["passed"], rep
+    assert np.isfinite(one.float().numpy()).all()

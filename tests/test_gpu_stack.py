@@ -99,24 +99,3 @@ def test_stack_validation():
     ok = P.prepare_stack(layers[:1])
     with pytest.raises(P.ShapeError):
         ok.forward(torch.zeros((1, 5, 4, 4), device="cuda"))
-
-
-def test_workspace_high_water():
-    """segb_workspace_high_water: K3 takes its NHWC operand copy from the device pool, K3b nothing"""
-    import torch
-    from paper_2502_20493_b200 import _lib
-    from paper_2502_20493_b200.synth import device_unit_floats
-    dev = torch.cuda.current_device()
-    k3 = P.prepare_layer(O.gen_kernel_bank(256, 128, 4, 3), 2, compute="bf16")      # 32x32 -> K3p / K3
-    k3b = P.prepare_layer(O.gen_kernel_bank(64, 64, 4, 4), 2, compute="bf16")       # 128-wide rows -> K3b
-    x = device_unit_floats((2, 256, 32, 32), 1, dtype=torch.bfloat16)
-    xb = device_unit_floats((2, 64, 64, 64), 2, dtype=torch.bfloat16)
-    k3b.forward(xb)
-    torch.cuda.synchronize()
-    _lib.workspace_high_water(dev, reset=True)
-    k3b.forward(xb)
-    torch.cuda.synchronize()
-    assert _lib.workspace_high_water(dev) == 0
-    k3.forward(x)
-    torch.cuda.synchronize()
-    assert _lib.workspace_high_water(dev) >= 2 * 256 * 32 * 32 * 2  # the NHWC bf16 copy of x

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_lib.SIGNATURES)
-    assert _lib.lib().segb_abi_version() == 1
+    assert _lib.lib().segb_abi_version() == 2
 
 
 def test_library_has_sm100a_code():

@@ -107,3 +107,16 @@ def test_compare_semantics(pad):
     assert not O.compare(a, b)["passed"]
     assert O.compare(a, b, 1e-2, 1e-6)["passed"]
     assert not O.compare(np.zeros((2, 2)), np.zeros((3, 3)))["shapes_match"]
+
+
+def test_counted_engines(golden):
+    """the scalar restatements (engines.py:353-406) reproduce the reference's counted engines
+    bit for bit, counters included"""
+    for i in range(int(golden["n_cnt"])):
+        m, k, pad = golden[f"cnt{i}_map"], golden[f"cnt{i}_kernel"], int(golden[f"cnt{i}_pad"])
+        c = golden[f"cnt{i}_counts"]
+        ref, rm, rw = O.forward_scalar_reference(m, k, pad)
+        seg, sm, sw = O.forward_scalar(m[None], k[None, None], pad)
+        assert np.array_equal(ref, golden[f"cnt{i}_ref"]), i
+        assert np.array_equal(seg[0], golden[f"cnt{i}_seg"]), i
+        assert (rm, rw, sm, sw) == tuple(int(v) for v in c), i

@@ -62,3 +62,27 @@ def test_gloo_world2_shard_and_gather(tmp_path, batch):
     mp.spawn(_worker, args=(2, _free_port(), batch, out), nprocs=2, join=True)
     full = torch.load(out)
     assert full.shape[0] == batch
+
+
+def _channel_worker(rank, world, port, c_out, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_20493_b200.parallel import gather_channels
+        g = torch.Generator().manual_seed(1)
+        y_full = torch.rand((3, c_out, 4, 5), generator=g)
+        co0, co1 = shard_range(c_out, world, rank)
+        full = gather_channels(y_full[:, co0:co1], c_out)
+        assert torch.equal(full, y_full)
+        if rank == 0:
+            torch.save(full, out_path)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("c_out", [5, 6])
+def test_gloo_world2_channel_gather(tmp_path, c_out):
+    out = str(tmp_path / "full.pt")
+    mp.spawn(_channel_worker, args=(2, _free_port(), c_out, out), nprocs=2, join=True)
+    assert torch.load(out).shape[1] == c_out
