@@ -106,13 +106,14 @@ def layer_stats(cfg, batch, dtype):
     return macs, nbytes, (oh, ow)
 
 
-def compute_roof(path: str, dtype: str, peaks: dict):
-    """(TFLOP/s, name) of the unit a layer's kernel computes on."""
-    if path == "igemm":
-        if dtype == "bf16":
-            return peaks["bf16_tflops"], "tensor (bf16, MEASURED_PEAKS)"
-        # fp32 on tensor cores: three kind::tf32 MMAs per product (3xTF32)
-        return peaks["tf32_mma_tflops"] / 3.0, "tensor (3xTF32: tf32 MMA ceiling / 3)"
+def compute_roof(kernel: str, peaks: dict):
+    """(TFLOP/s, name) of the unit a layer's kernel (segb_describe_path text) computes on."""
+    if kernel.startswith("K3"):
+        if "3xFP16" in kernel:  # fp32 as three kind::f16 MMAs per product on scaled fp16 hi/lo
+            return peaks["fp16_mma_tflops"] / 3.0, "tensor (3xFP16: fp16 MMA ceiling / 3, measured)"
+        if "3xTF32" in kernel:  # three kind::tf32 MMAs per product
+            return peaks["tf32_mma_tflops"] / 3.0, "tensor (3xTF32: tf32 MMA ceiling / 3, measured)"
+        return peaks["bf16_tflops"], "tensor (bf16, MEASURED_PEAKS)"
     return peaks["ffma_tflops"], "fp32 FFMA (measured)"
 
 
@@ -477,7 +478,7 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
         y = torch.empty((local, co, oh, ow), dtype=tdt, device=dev)
         state.append({"name": name, "cfg": cfg, "layer": layer, "x": x, "y": y, "macs": macs, "bytes": nbytes,
                       "bank": bank, "path": layer.select_path(_lib.BF16 if dtype == "bf16" else _lib.F32, local, h, w),
-                      "flops": 2 * macs})
+                      "kernel": layer.describe_path(local, h, w), "flops": 2 * macs})
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local_rank)
@@ -587,7 +588,7 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
     layer_rows = []
     for j, s in enumerate(state):
         lms = float(np.mean(per_layer[j]))
-        cpeak, cname = compute_roof(s["path"], dtype, peaks)
+        cpeak, cname = compute_roof(s["kernel"], peaks)
         t_comp = s["flops"] / (cpeak * 1e12)
         t_hbm = s["bytes"] / (peaks["hbm_gbs"] * 1e9)
         bound = "tensor" if (t_comp > t_hbm and s["path"] == "igemm") else ("ffma" if t_comp > t_hbm else "hbm")
@@ -595,7 +596,7 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
             achieved, peak, unit = s["flops"] / (lms * 1e-3) / 1e12, cpeak, "TFLOP/s"
         else:
             achieved, peak, unit = s["bytes"] / (lms * 1e-3) / 1e9, peaks["hbm_gbs"], "GB/s"
-        layer_rows.append({"name": s["name"], "path": s["path"], "ms": lms,
+        layer_rows.append({"name": s["name"], "path": s["path"], "kernel": s["kernel"], "ms": lms,
                            "gmacs": s["macs"] / (lms * 1e-3) / 1e9, "bound": bound, "peak_name": cname,
                            "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                            "alg_bytes": s["bytes"], "flops": s["flops"]})
@@ -606,7 +607,7 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
         with open(tpath) as f:
             traffic = json.load(f).get(workload, {}).get(dom["name"])
     roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-                "frac": dom["frac"], "traffic": traffic, "kernel": f"{dom['name']} ({dom['path']})",
+                "frac": dom["frac"], "traffic": traffic, "kernel": f"{dom['name']}: {dom['kernel']}",
                 "share_of_step": dom["ms"] / ms, "peak_source": dom["peak_name"] if dom["bound"] != "hbm"
                 else peaks["source"]}
 
@@ -689,7 +690,7 @@ def run_ours(args, rank, world, local_rank):
         companion = {"workload": COMPANION[wl], "dtype": "bf16", "value": c["value"], "unit": "GMAC/s",
                      "ms_per_step": c["ms_per_step"], "roofline": c["roofline"], "parity": c["parity"],
                      "e2e": c["e2e"], "gpu_launches": c["gpu_launches"], "clocks": c["clocks"],
-                     "layers": [{k: row[k] for k in ("name", "path", "ms", "gmacs", "bound", "frac")}
+                     "layers": [{k: row[k] for k in ("name", "kernel", "ms", "gmacs", "bound", "frac")}
                                 for row in c["layers"]]}
     if rank != 0:
         return 0
@@ -712,8 +713,9 @@ def run_ours(args, rank, world, local_rank):
            "data": "synthetic (reference splitmix64 generator, produced on device)",
            "config": {"workload": wl, "batch_per_gpu": r["local_batch"], "total_batch": r["batch"] if scaling ==
                       "strong" else r["batch"] * world, "layers": [c[0] for c in layers],
-                      "precision": ("fp32 in/out; tensor-core layers as 3xTF32 (hi*hi + hi*lo + lo*hi), direct "
-                                    "layers FFMA; gate rel 1e-5 / abs 1e-6" if dtype == "fp32" else
+                      "precision": ("fp32 in/out; tensor-core layers as 3xFP16 (power-of-two scaled fp16 hi/lo "
+                                    "planes, hi*hi + hi*lo + lo*hi in fp32, unscaled exactly), direct layers FFMA; "
+                                    "gate rel 1e-5 / abs 1e-6" if dtype == "fp32" else
                                     "bf16 operands, fp32 accumulation, bf16 out"),
                       "launch": "eager" if args.no_graph else
                       "one CUDA graph per step (per-layer graphs for the layer breakdown)", "l2": flush_note},

@@ -139,6 +139,11 @@ int segb_forward_ws(const segb_layer *layer, const void *x, int x_dtype, int64_t
  * on this layer, so concurrent streams should use segb_forward_ws instead). */
 int segb_layer_reserve_workspace(segb_layer *layer, int64_t bytes);
 
+/* the kernel family (and operand mode) this call runs, as text, e.g.
+ * "K3 implicit GEMM (3xFP16)" or "K3b row-streaming GEMM (bf16)" */
+int segb_describe_path(const segb_layer *layer, int x_dtype, int64_t batch, int in_h, int in_w, int y_dtype,
+                       int compute_dtype, int path, char *buf, int buf_len);
+
 /* which kernel SEGB_PATH_AUTO picks for this call (SEGB_PATH_DIRECT/IGEMM) */
 int segb_select_path(const segb_layer *layer, int x_dtype, int64_t batch, int in_h, int in_w,
                      int compute_dtype);

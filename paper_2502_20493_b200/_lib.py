@@ -41,6 +41,7 @@ SIGNATURES = {
     "segb_forward_workspace_bytes": (_i, [_p, _i, _i64, _i, _i, _i, _i, _i, ctypes.POINTER(_i64)]),
     "segb_forward_ws": (_i, [_p, _p, _i, _i64, _i, _i, _p, _i, _i, _i, _p, _i64, _p]),
     "segb_layer_reserve_workspace": (_i, [_p, _i64]),
+    "segb_describe_path": (_i, [_p, _i, _i64, _i, _i, _i, _i, _i, ctypes.c_char_p, _i]),
     "segb_stack_workspace_bytes": (_i, [ctypes.POINTER(_p), _i, _i64, _i, _i, _i, ctypes.POINTER(_i64)]),
     "segb_stack_workspace_bytes2": (_i, [ctypes.POINTER(_p), _i, _i64, _i, _i, _i, _i, _i,
                                          ctypes.POINTER(_i64)]),

@@ -4,6 +4,7 @@
 
 #include "common.cuh"
 #include "direct_impl.cuh"
+#include "f16split.cuh"
 #include "igemm.cuh"
 #include "kernels.cuh"
 
@@ -70,6 +71,8 @@ struct segb_layer {
     int n2p = 0;
     void *wg = nullptr;  // K3 weights (bf16, class/tap-major, K-major)
     void *wt = nullptr;  // K3 3xTF32 weights: fp32 hi plane followed by the lo plane
+    void *wf = nullptr;  // K3 3xFP16 weights: fp16 hi plane, lo plane, then the bank's absmax partials
+    int f16_wexp = 0;    // their scale exponent k_w (weights were multiplied by 2^k_w)
     int c_in_pad = 0, c_out_pad = 0, c_in_pad32 = 0;  // zero-padded GEMM operand extents
     void *wz = nullptr;  // K3c weights (bf16, (kx, ky, co) rows x 64-padded c_in, K-major)
     void *ws = nullptr;  // workspace reserved by segb_layer_reserve_workspace (segb_forward)
@@ -165,6 +168,35 @@ static int ensure_tf32_weights(segb_layer *L, bool lazy, cudaStream_t st) {
     });
 }
 
+static size_t f16_plane(const segb_layer *L) { return (size_t)L->n * L->n * L->c_out_pad * L->c_in_pad; }
+
+// 3xFP16 weights; the scale exponent is read back once (prepare is synchronous on its stream)
+static int ensure_f16x3_weights(segb_layer *L, bool lazy, cudaStream_t st) {
+    const size_t plane = f16_plane(L);
+    const size_t bytes = 2 * 2 * plane + 1024;
+    int rc = ensure_layout(L, &L->wf, bytes, lazy, st, "3xFP16 implicit-GEMM", [&](void *p) -> int {
+        float *partials = (float *)((char *)p + 4 * plane);
+        int r = run_prep_gemm_f16x2(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->c_out_pad, L->n, p,
+                                    (char *)p + 2 * plane, partials, st);
+        if (r) return r;
+        float hp[kAbsmaxBlocks];
+        cudaError_t e = cudaMemcpyAsync(hp, partials, sizeof hp, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(SEGB_ERR_CUDA, "3xFP16 weight scale: %s", cudaGetErrorString(e));
+        float m = 0.f;
+        for (float v : hp) m = std::max(m, v);
+        L->f16_wexp = f16_scale_exp(m);
+        return (int)SEGB_OK;
+    });
+    return rc;
+}
+
+// fp32 tensor-core mode: 3xFP16 unless SEGB200_FP32_TC=tf32x3 (A/B switch, read at prepare)
+static bool want_tf32x3() {
+    const char *e = getenv("SEGB200_FP32_TC");
+    return e && std::string(e) == "tf32x3";
+}
+
 // weight-only conditions under which the dispatcher can pick each tensor-core path (the shape
 // conditions of igemm_supported that do not depend on the input)
 static bool may_use_gemm_bf16(const segb_layer *L) {
@@ -173,6 +205,10 @@ static bool may_use_gemm_bf16(const segb_layer *L) {
 static bool may_use_scatter(const segb_layer *L) {
     return L->engine == SEGB_ENGINE_SEGREGATED && L->c_in >= 64 && L->c_in <= 256 &&
            L->n * L->n * L->c_out <= 256 && L->n <= 8 && 4 * L->c_out <= L->c_in && igemm_available();
+}
+static bool may_use_f16x3(const segb_layer *L) {
+    return L->engine == SEGB_ENGINE_SEGREGATED && L->n % 2 == 0 && L->c_in >= 64 && L->c_in % 8 == 0 &&
+           L->c_out >= 16 && igemm_available();
 }
 static bool may_use_tf32(const segb_layer *L) {
     return L->engine == SEGB_ENGINE_SEGREGATED && L->n % 2 == 0 && L->c_in >= 32 && L->c_in % 4 == 0 &&
@@ -188,6 +224,7 @@ static bool igemm_ok(const segb_layer *L, int x_dtype, int64_t batch, int in_h, 
     IgemmShape s{};
     s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
     s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.compute = compute;
+    s.f16x3 = compute == SEGB_F32 && L->wf != nullptr;
     return igemm_supported(s);
 }
 
@@ -289,7 +326,8 @@ int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int n, i
     int rc = ensure_direct_weights(L, compute, false, st, nullptr);
     if (!rc && compute == SEGB_BF16 && may_use_gemm_bf16(L)) rc = ensure_gemm_weights(L, false, st);
     if (!rc && compute == SEGB_BF16 && may_use_scatter(L)) rc = ensure_scatter_weights(L, false, st);
-    if (!rc && compute == SEGB_F32 && may_use_tf32(L)) rc = ensure_tf32_weights(L, false, st);
+    if (!rc && compute == SEGB_F32 && may_use_f16x3(L) && !want_tf32x3()) rc = ensure_f16x3_weights(L, false, st);
+    if (!rc && compute == SEGB_F32 && may_use_tf32(L) && !L->wf) rc = ensure_tf32_weights(L, false, st);
     if (rc) {
         segb_release(L);
         return rc;
@@ -345,8 +383,12 @@ static int plan_forward(const segb_layer *L, int x_dtype, int64_t batch, int in_
         s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
         s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.compute = compute;
         s.c_out_pad = L->c_out_pad;
-        if (compute == SEGB_F32) s.c_in_pad32 = L->c_in_pad32;
-        else s.c_in_pad = L->c_in_pad;
+        s.c_in_pad = L->c_in_pad;
+        s.c_in_pad32 = L->c_in_pad32;
+        if (compute == SEGB_F32 && L->wf) {
+            s.f16x3 = 1;
+            s.w_exp = L->f16_wexp;
+        }
         pl.ws_bytes = igemm_workspace_bytes(s);
     }
     return SEGB_OK;
@@ -366,6 +408,8 @@ static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch
     const int oh = pl.oh, ow = pl.ow;
     if (pl.path == SEGB_PATH_IGEMM) {
         IgemmShape &s = pl.s;
+        if (compute == SEGB_F32 && s.f16x3) return run_igemm(s, x, L->wf, (const char *)L->wf + 2 * f16_plane(L), y, ws,
+                                                             ws_bytes, st);
         if (compute == SEGB_F32) {
             if (int rc = ensure_tf32_weights(L, true, st)) return rc;
             return run_igemm(s, x, L->wt, (const char *)L->wt + 4 * tf32_plane(L), y, ws, ws_bytes, st);
@@ -398,6 +442,18 @@ static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch
             return launch_direct_f64(a, ref, st);
         default: return launch_direct_bf16(a, x_dtype, y_dtype, ref, st);
     }
+}
+
+int segb_describe_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int y_dtype,
+                       int compute, int path, char *buf, int buf_len) {
+    FwdPlan pl;
+    if (int rc = plan_forward(L, x_dtype, batch, in_h, in_w, y_dtype, compute, path, pl)) return rc;
+    const char *name = "K2 direct (fp32 FFMA)";
+    if (pl.path == SEGB_PATH_IGEMM) name = igemm_kernel_name(pl.s);
+    else if (pl.compute == SEGB_F64) name = "K2 direct (fp64)";
+    else if (pl.compute == SEGB_BF16) name = "K2 direct (bf16 operands, fp32 FFMA)";
+    if (buf && buf_len > 0) snprintf(buf, (size_t)buf_len, "%s", name);
+    return SEGB_OK;
 }
 
 int segb_forward_workspace_bytes(const segb_layer *L, int x_dtype, int64_t batch, int in_h, int in_w, int y_dtype,
@@ -537,6 +593,7 @@ int segb_release(segb_layer *L) {
     cudaFree(L->wg);
     cudaFree(L->wt);
     cudaFree(L->wz);
+    cudaFree(L->wf);
     cudaFree(L->ws);
     delete L;
     return SEGB_OK;

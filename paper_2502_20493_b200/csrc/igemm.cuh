@@ -8,11 +8,14 @@ namespace segb {
 struct IgemmShape {
     int64_t batch;
     int c_in, c_out, h, w, n, pad, x_dtype, y_dtype, c_in_pad, c_out_pad, c_in_pad32;
-    int compute;  // SEGB_BF16 (kind::f16) or SEGB_F32 (3xTF32, kind::tf32)
+    int compute;  // SEGB_BF16 (kind::f16) or SEGB_F32 (3xFP16 on kind::f16, or 3xTF32 on kind::tf32)
+    int f16x3;    // fp32 compute as 3xFP16 (weights: scaled fp16 hi / lo planes)
+    int w_exp;    // 3xFP16: the weight planes' scale exponent k_w
 };
 
 bool igemm_available();
 bool igemm_supported(const IgemmShape &s);
+const char *igemm_kernel_name(const IgemmShape &s);  // the kernel family run_igemm picks
 // workspace (bytes) run_igemm needs for this shape: K3's NHWC operand copy or K3c's tap products
 int64_t igemm_workspace_bytes(const IgemmShape &s);
 int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,

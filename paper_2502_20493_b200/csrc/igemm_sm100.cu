@@ -46,6 +46,12 @@ template <int MODE> constexpr int kstep_channels() { return MODE == kModeTf32x3 
 // of accumulate steps (measured on B200: ~0.25 ulp per MMA), so every kTf32Chunk k-steps
 // (96 MMAs) the partial is moved into fp32 registers.
 constexpr int kTf32Chunk = 8;
+// 3xFP16 k-steps hold twice the channels (the same 12 MMAs per k-step); its partials are drained
+// every 4 k-steps (48 MMAs): measured max rel vs the fp64 oracle 5e-6 with 8 (B=256 EB-GAN)
+#ifndef SEGB_F16X3_CHUNK
+#define SEGB_F16X3_CHUNK 4
+#endif
+constexpr int kF16Chunk = SEGB_F16X3_CHUNK;
 constexpr int kTf32MaxN = 128;
 
 // instruction descriptor: fp16 x fp16 -> fp32, A and B K-major, M = 128, N = n
@@ -102,6 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr bool TFK = MODE == kModeTf32x3;   // kind::tf32 MMAs
     constexpr int KCH = kstep_channels<MODE>();
     constexpr int NOP = TF32X3 ? 2 : 1;  // tiles per operand per stage (hi [, lo])
+    constexpr int CHUNK = MODE == kModeF16x3 ? kF16Chunk : kTf32Chunk;  // k-steps per TMEM partial
     constexpr bool PAIR = PM > 0, TWO = PM == 2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B atoms
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ks = 0; ks < ksteps; ++ks) {
                     // 3xTF32 accumulates at most kTf32Chunk k-steps per TMEM partial (the
                     // epilogue sums partials in fp32 registers, round-to-nearest)
-                    const int kc = TF32X3 ? ks % kTf32Chunk : ks;
+                    const int kc = TF32X3 ? ks % CHUNK : ks;
                     if (kc == 0) {
                         if (ks > 0) {
                             commit(&tfull[acc], false);
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t lt[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
             for (int t = t_begin; t < prm.total_tiles; t += t_step) {
                 const ClassGeom &g = prm.cls[t & 3];
-                const int uses = TF32X3 ? (g.R * g.C * prm.k_cblocks + kTf32Chunk - 1) / kTf32Chunk : 1;
+                const int uses = TF32X3 ? (g.R * g.C * prm.k_cblocks + CHUNK - 1) / CHUNK : 1;
                 for (int k = 0; k < uses; ++k) {
                     mbar_wait(&tempty[acc], acc_phase);
                     mbar_arrive_cluster(lt[acc]);
@@ -322,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int c, mb, nb;
             decode(t, c, mb, nb);
             const ClassGeom &g = prm.cls[c];
-            const int nchunks = (g.R * g.C * prm.k_cblocks + kTf32Chunk - 1) / kTf32Chunk;
+            const int nchunks = (g.R * g.C * prm.k_cblocks + CHUNK - 1) / CHUNK;
             float racc[kTf32MaxN];
 #pragma unroll
             for (int k = 0; k < kTf32MaxN; ++k) racc[k] = 0.f;
@@ -508,10 +515,95 @@ __global__ void nchw_to_nhwc_tf32x2(const float *__restrict__ x, float *__restri
     }
 }
 
+// NCHW fp32 -> NHWC fp16 hi / lo planes of the 3xFP16 A operand, scaled by 2^k_x (k_x from the
+// input's absmax partials, f16split.cuh). Thread (cg = t & 7, hc = t >> 3) of a 256-thread block
+// loads an 8-channel x 8-position tile with 128-bit loads, splits it and transposes the fp16 pairs
+// in registers (byte permutes) into 8 channels-last 16-byte rows per plane. HW % 8 == 0, C % 8 == 0.
+__global__ void __launch_bounds__(256) nchw_to_nhwc_f16x2_v8(const float *__restrict__ x, __half *__restrict__ hi,
+                                                              __half *__restrict__ lo, int C, int HW,
+                                                              const float *__restrict__ partials) {
+    __shared__ float scale;
+    if (threadIdx.x < 32) {
+        float m = 0.f;
+        for (int i = threadIdx.x; i < kAbsmaxBlocks; i += 32) m = fmaxf(m, __ldg(partials + i));
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (threadIdx.x == 0) scale = ldexpf(1.f, f16_scale_exp(m));
+    }
+    __syncthreads();
+    const float sc = scale;
+    const int64_t b = blockIdx.z;
+    const int cg = threadIdx.x & 7, hc = threadIdx.x >> 3;
+    const int c0 = blockIdx.y * 64 + cg * 8;
+    const int hw0 = blockIdx.x * 256 + hc * 8;
+    if (c0 >= C || hw0 >= HW) return;
+    const float *src = x + (b * C + c0) * (int64_t)HW + hw0;
+    uint32_t rh[8][4], rl[8][4];  // [channel][k]: positions 2k, 2k+1 as fp16 pairs
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)c * HW));
+        const float4 bb = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)c * HW + 4));
+        const float v[8] = {a.x, a.y, a.z, a.w, bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            __half h0, l0, h1, l1;
+            split_f16(v[2 * k] * sc, h0, l0);
+            split_f16(v[2 * k + 1] * sc, h1, l1);
+            rh[c][k] = pack_h2(h0, h1);
+            rl[c][k] = pack_h2(l0, l1);
+        }
+    }
+    const int64_t off = (b * HW + hw0) * (int64_t)C + c0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        uint4 oh, ol;
+        uint32_t *ph = &oh.x, *pl = &ol.x;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const uint32_t sel = (w & 1) ? 0x7632 : 0x5410;
+            ph[m] = __byte_perm(rh[2 * m][w >> 1], rh[2 * m + 1][w >> 1], sel);
+            pl[m] = __byte_perm(rl[2 * m][w >> 1], rl[2 * m + 1][w >> 1], sel);
+        }
+        *reinterpret_cast<uint4 *>(hi + off + (int64_t)w * C) = oh;
+        *reinterpret_cast<uint4 *>(lo + off + (int64_t)w * C) = ol;
+    }
+}
+
+// generic-shape 3xFP16 staging: one element per thread, NHWC-indexed (coalesced stores)
+__global__ void nchw_to_nhwc_f16x2(const float *__restrict__ x, __half *__restrict__ hi, __half *__restrict__ lo, int C,
+                                   int HW, int64_t total, const float *__restrict__ partials) {
+    __shared__ float scale;
+    if (threadIdx.x < 32) {
+        float m = 0.f;
+        for (int i = threadIdx.x; i < kAbsmaxBlocks; i += 32) m = fmaxf(m, __ldg(partials + i));
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (threadIdx.x == 0) scale = ldexpf(1.f, f16_scale_exp(m));
+    }
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % C);
+        const int64_t bhw = e / C;
+        const int64_t b = bhw / HW, hw = bhw % HW;
+        __half h, l;
+        split_f16(__ldg(x + (b * C + c) * HW + hw) * scale, h, l);
+        hi[e] = h;
+        lo[e] = l;
+    }
+}
+
+static int fp32_mode(const IgemmShape &s) {
+    if (s.compute != SEGB_F32) return kModeBf16;
+    return s.f16x3 ? kModeF16x3 : kModeTf32x3;
+}
+
 static bool make_params(const IgemmShape &s, IgemmParams &prm) {
-    const bool tf32 = s.compute == SEGB_F32;
+    const int mode = fp32_mode(s);
+    const bool tf32 = mode != kModeBf16;  // three-pass operands (hi / lo planes)
     if (s.n % 2 != 0) return false;  // all four classes share one grid
-    if (tf32) {
+    if (mode == kModeF16x3) {
+        if (s.c_in < 64 || s.c_in % 8 != 0) return false;
+        if (s.c_out < 16) return false;
+        if (s.x_dtype != SEGB_F32 || s.y_dtype != SEGB_F32) return false;
+    } else if (tf32) {
         if (s.c_in < 32 || s.c_in % 4 != 0) return false;
         if (s.c_out < 16) return false;  // >2x padded N x 3 passes: the FFMA direct kernel is faster
         if (s.x_dtype != SEGB_F32 || s.y_dtype != SEGB_F32) return false;
@@ -579,7 +671,7 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     prm.n_tile = nt;
     prm.n_blocks = cop / nt;
     prm.batch = (int)s.batch; prm.c_in = s.c_in; prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
-    const int kch = tf32 ? 32 : 64;
+    const int kch = mode == kModeTf32x3 ? 32 : 64;
     prm.k_cblocks = (s.c_in + kch - 1) / kch;
     prm.class_positions = s.batch * (int64_t)rows * cols;
     prm.m_tiles = (int)ceil_div(prm.class_positions, kBlockM);
@@ -602,15 +694,26 @@ bool igemm_supported(const IgemmShape &s) {
     return igemm_scatter_supported(s) || use_rows(s) || (make_params(s, prm) && tensor_map_encoder() != nullptr);
 }
 
+const char *igemm_kernel_name(const IgemmShape &s) {
+    if (igemm_scatter_supported(s)) return "K3c scatter-GEMM + gather (bf16)";
+    if (use_rows(s)) return "K3b row-streaming GEMM (bf16)";
+    const int mode = fp32_mode(s);
+    if (mode == kModeF16x3) return "K3 implicit GEMM (3xFP16)";
+    if (mode == kModeTf32x3) return "K3 implicit GEMM (3xTF32)";
+    if (igemm_cp_supported(s)) return "K3p class-pair GEMM (bf16)";
+    return "K3 implicit GEMM (bf16)";
+}
+
 // K3's only workspace: the channels-last A operand (bf16, or fp32 hi followed by fp32 lo for
 // 3xTF32), written by the staging launch and read by the GEMM. K3b and K3c's own kernels take
 // none from here (K3c's tap products are counted by igemm_scatter_workspace_bytes).
 int64_t igemm_workspace_bytes(const IgemmShape &s) {
     if (igemm_scatter_supported(s)) return igemm_scatter_workspace_bytes(s);
     if (use_rows(s)) return 0;
-    const bool tf32 = s.compute == SEGB_F32;
+    const int mode = fp32_mode(s);
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
-    return (elems * (tf32 ? 8 : 2) + 255) / 256 * 256;
+    const int64_t bpe = mode == kModeTf32x3 ? 8 : (mode == kModeF16x3 ? 4 : 2);  // bytes per element, all planes
+    return (elems * bpe + 255) / 256 * 256 + (mode == kModeF16x3 ? 1024 : 0);   // + the absmax partials
 }
 
 static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const void *ptr, const cuuint64_t *dims,
@@ -622,10 +725,10 @@ static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const vo
     return r == CUDA_SUCCESS ? SEGB_OK : fail(SEGB_ERR_CUDA, "tensor map %s: error %d", what, (int)r);
 }
 
-template <typename TY, bool TF32X3, int PM>
+template <typename TY, int MODE, int PM>
 static int launch_k3(unsigned grid, size_t smem, cudaStream_t st, const CUtensorMap &tmA, const CUtensorMap &tmB,
                      const CUtensorMap &tmAlo, const CUtensorMap &tmBlo, const IgemmParams &prm) {
-    auto kern = igemm_tconv_kernel<TY, TF32X3, PM>;
+    auto kern = igemm_tconv_kernel<TY, MODE, PM>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (PM == 0) {
         kern<<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
@@ -653,17 +756,30 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     IgemmParams prm;
     if (!make_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM: unsupported shape");
     if (!tensor_map_encoder()) return fail(SEGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const bool tf32 = s.compute == SEGB_F32;
+    const int mode = fp32_mode(s);
+    const bool tf32 = mode != kModeBf16;  // hi / lo planes
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
-    const int esz = tf32 ? 4 : 2;
+    const int esz = mode == kModeTf32x3 ? 4 : 2;
     void *xs = ws;  // channels-last A operand in the caller's workspace
     if (!xs || ws_bytes < igemm_workspace_bytes(s))
         return fail(SEGB_ERR_VALUE, "implicit GEMM: workspace of %lld bytes needed, got %lld",
                     (long long)igemm_workspace_bytes(s), (long long)ws_bytes);
     void *xs_lo = tf32 ? (void *)((char *)xs + elems * esz) : nullptr;
+    float *partials = mode == kModeF16x3 ? (float *)((char *)xs + (2 * elems * esz + 255) / 256 * 256) : nullptr;
     {
         const int hw = s.h * s.w;
-        if (tf32) {
+        if (mode == kModeF16x3) {
+            if (int rc = run_absmax_partials(x, SEGB_F32, elems, partials, st)) return rc;
+            if (hw % 8 == 0 && s.c_in % 8 == 0) {
+                dim3 grd((unsigned)ceil_div(hw, 256), (unsigned)ceil_div(s.c_in, 64), (unsigned)s.batch);
+                nchw_to_nhwc_f16x2_v8<<<grd, 256, 0, st>>>((const float *)x, (__half *)xs, (__half *)xs_lo, s.c_in, hw,
+                                                           partials);
+            } else {
+                const unsigned g = (unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 64);
+                nchw_to_nhwc_f16x2<<<g, 256, 0, st>>>((const float *)x, (__half *)xs, (__half *)xs_lo, s.c_in, hw, elems,
+                                                      partials);
+            }
+        } else if (tf32) {
             const unsigned g = (unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 64);
             nchw_to_nhwc_tf32x2<<<g, 256, 0, st>>>((const float *)x, (float *)xs, (float *)xs_lo, s.c_in, hw, elems);
         } else if (hw % 8 == 0 && s.c_in % 8 == 0) {
@@ -687,9 +803,11 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     if (!tf32 && igemm_cp_supported(s)) {  // K3p: both column parities per tile
         return run_igemm_cp_core(s, xs, wg, y, st);
     }
-    const int kch = tf32 ? 32 : 64;
-    const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    const int cin_pad = tf32 ? s.c_in_pad32 : s.c_in_pad;
+    const int kch = mode == kModeTf32x3 ? 32 : 64;
+    const CUtensorMapDataType dt = mode == kModeTf32x3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : mode == kModeF16x3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                        : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const int cin_pad = mode == kModeTf32x3 ? s.c_in_pad32 : s.c_in_pad;
     CUtensorMap tmA, tmB, tmAlo, tmBlo;
     cuuint64_t adims[4] = {(cuuint64_t)s.c_in, (cuuint64_t)s.w, (cuuint64_t)s.h, (cuuint64_t)s.batch};
     cuuint64_t astr[3] = {(cuuint64_t)s.c_in * esz, (cuuint64_t)s.w * s.c_in * esz, (cuuint64_t)s.h * s.w * s.c_in * esz};
@@ -719,6 +837,8 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     if (rc) return rc;
     if (!tf32) { tmAlo = tmA; tmBlo = tmB; }
     prm.y = y;
+    prm.x_partials = partials;
+    prm.w_unscale = ldexpf(1.f, -s.w_exp);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -731,12 +851,14 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     rc = pm == 2   ? launch_k3<TY_, TF_, 2>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
          : pm == 1 ? launch_k3<TY_, TF_, 1>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
                    : launch_k3<TY_, TF_, 0>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm);
-    if (tf32) {
-        SEGB_K3_LAUNCH(float, true)
+    if (mode == kModeF16x3) {
+        SEGB_K3_LAUNCH(float, kModeF16x3)
+    } else if (mode == kModeTf32x3) {
+        SEGB_K3_LAUNCH(float, kModeTf32x3)
     } else if (s.y_dtype == SEGB_BF16) {
-        SEGB_K3_LAUNCH(__nv_bfloat16, false)
+        SEGB_K3_LAUNCH(__nv_bfloat16, kModeBf16)
     } else {
-        SEGB_K3_LAUNCH(float, false)
+        SEGB_K3_LAUNCH(float, kModeBf16)
     }
 #undef SEGB_K3_LAUNCH
     if (rc) return rc;

@@ -181,7 +181,6 @@ class PreparedLayer:
             ctypes.byref(handle)))
         self._handle = handle
         self._lib = _lib.lib()
-        self._ws_cache: dict = {}
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -361,6 +360,21 @@ class PreparedLayer:
             main.synchronize()
         return out_h_t
 
+    def describe_path(self, batch: int, in_h: int, in_w: int, x_dtype=None, y_dtype=None,
+                      compute: str | None = None, path: str = "auto") -> str:
+        """The kernel family (and operand mode) a forward of this shape runs (segb_describe_path)."""
+        t = _device.torch()
+        compute = compute or self.compute
+        if x_dtype is None:
+            x_dtype = t.bfloat16 if compute == "bf16" else (t.float64 if compute == "fp64" else t.float32)
+        if y_dtype is None:
+            y_dtype = x_dtype
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(self._lib.segb_describe_path(self._handle, _device.dtype_id(x_dtype), int(batch), int(in_h),
+                                                int(in_w), _device.dtype_id(y_dtype), COMPUTE_DTYPES[compute],
+                                                _lib.PATH_IDS[path], buf, 128))
+        return buf.value.decode()
+
     def workspace_bytes(self, batch: int, in_h: int, in_w: int, x_dtype=None, y_dtype=None,
                         compute: str | None = None, path: str = "auto") -> int:
         """Device scratch bytes one forward of this shape takes (segb_forward_workspace_bytes):
@@ -375,14 +389,10 @@ class PreparedLayer:
                               int(in_w), COMPUTE_DTYPES[compute], _lib.PATH_IDS[path])
 
     def _ws_bytes(self, xd, yd, b, h, w, cid, pid) -> int:
-        key = (xd, yd, b, h, w, cid, pid)
-        v = self._ws_cache.get(key)
-        if v is None:
-            r = ctypes.c_int64()
-            _lib.check(self._lib.segb_forward_workspace_bytes(self._handle, xd, b, h, w, yd, cid, pid,
-                                                              ctypes.byref(r)))
-            v = self._ws_cache[key] = int(r.value)
-        return v
+        # not cached: the kernel choice (and so the scratch) can follow A/B environment switches
+        r = ctypes.c_int64()
+        _lib.check(self._lib.segb_forward_workspace_bytes(self._handle, xd, b, h, w, yd, cid, pid, ctypes.byref(r)))
+        return int(r.value)
 
     def _launch(self, d_x, d_y, compute: str, path: str) -> None:
         """One segb_forward_ws call on the caller's current stream. The workspace (if the kernel

@@ -156,7 +156,7 @@ def test_igemm_rows_variant(name, h, w, ci, n, co, pad, b, monkeypatch):
     assert O.compare(yb, y32.astype(np.float64), 2 ** -8 + 1e-4, 1e-6 * float(np.abs(ref).max()))["passed"], name
 
 
-TF32_CASES = [  # fp32 layers on tensor cores as 3xTF32 (kind::tf32): the reference's fp32 gate
+TF32_CASES = [  # fp32 layers on tensor cores (3xFP16 where c_in >= 64, else 3xTF32): the reference's fp32 gate
     ("ebgan_l2", 4, 4, 2048, 4, 1024, 2, 8),
     ("ebgan_l5", 32, 32, 256, 4, 128, 2, 2),
     ("ebgan_l7", 128, 128, 64, 4, 64, 2, 1),
@@ -165,16 +165,22 @@ TF32_CASES = [  # fp32 layers on tensor cores as 3xTF32 (kind::tf32): the refere
 ]
 
 
+@pytest.mark.parametrize("mode", ["3xFP16", "3xTF32"])
 @pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", TF32_CASES)
-def test_igemm_3xtf32_fp32_tolerance(name, h, w, ci, n, co, pad, b):
+def test_igemm_3xtf32_fp32_tolerance(monkeypatch, mode, name, h, w, ci, n, co, pad, b):
     """fp32 compute on the tensor-core path must still meet rel 1e-5 / abs 1e-6 against the
-    reference's fp32 engine inputs (oracle evaluated in fp64)."""
+    reference's fp32 engine inputs (oracle evaluated in fp64), in both operand modes
+    (SEGB200_FP32_TC=tf32x3 forces 3xTF32 at prepare)."""
     import torch
     from paper_2502_20493_b200.synth import device_unit_floats
+    if mode == "3xTF32":
+        monkeypatch.setenv("SEGB200_FP32_TC", "tf32x3")
     x = device_unit_floats((b, ci, h, w), 900 + ci, dtype=torch.float32)
     bank = O.gen_kernel_bank(ci, co, n, 901 + ci)
     layer = P.prepare_layer(bank, pad)  # compute = fp32 (the reference's working precision)
     assert layer.select_path(0, b, h, w) == "igemm", name
+    want = mode if (mode == "3xTF32" or ci >= 64) else "3xTF32"
+    assert want in layer.describe_path(b, h, w), (name, layer.describe_path(b, h, w))
     y = layer.forward(x, path="igemm").cpu().numpy()
     ref = O.forward_segregated_batch(x.cpu().numpy().astype(np.float64), bank.astype(np.float64), pad)
     rep = O.compare(y, ref, 1e-5, 1e-6)
@@ -296,3 +302,51 @@ def test_opt_in_variants(monkeypatch, env, val, shape, bitwise):
         ref = want32.cpu().numpy().astype(np.float64)
         assert O.compare(got32.cpu().numpy(), ref, 1e-5, 1e-6)["passed"], (env, val, shape)
         assert O.compare(got.float().cpu().numpy(), ref, 2 ** -7, 1e-3 * float(np.abs(ref).max()))["passed"]
+
+
+@pytest.mark.parametrize("xs,ws", [(1e-6, 1.0), (1.0, 1e-4), (3e4, 1.0), (1e6, 1e3), (2.0 ** -60, 2.0 ** 40)])
+def test_3xfp16_scales_follow_magnitudes(xs, ws):
+    """3xFP16 scales each operand by a power of two from its own maximum, so inputs far outside
+    fp16's range (tiny, huge) keep the reference's fp32 gate (relative to the output scale)."""
+    import torch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    b, ci, h, w, n, co, pad = 2, 128, 16, 16, 4, 64, 2
+    x = device_unit_floats((b, ci, h, w), 31, dtype=torch.float32) * xs
+    bank = (O.gen_kernel_bank(ci, co, n, 32) * ws).astype(np.float32)
+    layer = P.prepare_layer(bank, pad)
+    assert "3xFP16" in layer.describe_path(b, h, w)
+    y = layer.forward(x).cpu().numpy()
+    ref = O.forward_segregated_batch(x.cpu().numpy().astype(np.float64), bank.astype(np.float64), pad)
+    scale = float(np.abs(ref).max())
+    rep = O.compare(y, ref, 1e-5, 1e-6 * scale)
+    assert rep["passed"], (xs, ws, rep)
+
+
+def test_3xfp16_signed_data_error_bound():
+    """signed N(0,1) data cancels: gate each element against 1e-5 x sum|x||w| (the
+    conv of the magnitudes), the bound the reference's own fp32 engines meet on such data."""
+    import torch
+    b, ci, h, w, n, co, pad = 2, 256, 8, 8, 4, 128, 2
+    rng = np.random.default_rng(5)
+    xh = rng.standard_normal((b, ci, h, w)).astype(np.float32)
+    bank = rng.standard_normal((ci, co, n, n)).astype(np.float32)
+    layer = P.prepare_layer(bank, pad)
+    assert "3xFP16" in layer.describe_path(b, h, w)
+    y = layer.forward(torch.from_numpy(xh).cuda()).cpu().numpy().astype(np.float64)
+    ref = O.forward_segregated_batch(xh.astype(np.float64), bank.astype(np.float64), pad)
+    mag = O.forward_segregated_batch(np.abs(xh).astype(np.float64), np.abs(bank).astype(np.float64), pad)
+    assert np.all(np.abs(y - ref) <= 1e-5 * mag + 1e-6), float((np.abs(y - ref) / mag).max())
+
+
+def test_3xfp16_nan_propagates():
+    import torch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    x = device_unit_floats((1, 64, 8, 8), 3, dtype=torch.float32)
+    x[0, 5, 3, 4] = float("nan")
+    layer = P.prepare_layer(O.gen_kernel_bank(64, 32, 4, 4), 2)
+    assert "3xFP16" in layer.describe_path(1, 8, 8)
+    y = layer.forward(x).cpu().numpy()
+    ref = O.forward_segregated_batch(x.cpu().numpy().astype(np.float64), O.gen_kernel_bank(64, 32, 4, 4).astype(np.float64), 2)
+    assert np.array_equal(np.isnan(y), np.isnan(ref))
+    fin = ~np.isnan(ref)
+    assert O.compare(y[fin], ref[fin], 1e-5, 1e-6)["passed"]
