@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "f16split.cuh"
 #include "igemm.cuh"
 #include "tc_ptx.cuh"
 
@@ -75,6 +76,11 @@ struct RowsParams {
     void *y;
     unsigned long long *prof;  // optional role cycle counters (CTA 0), SEGB200_PROFILE=1
     int ablate;                // SEGB200_ABLATE bits, see ABL()
+    // F16 (3xFP16, fp32 in / out): every slot and weight tile holds an fp16 hi plane and a lo
+    // plane (f16split.cuh); the input's scale comes from its absmax partials
+    uint32_t slot_plane, b_plane;  // byte offset of the lo plane in a slot / in the weight area
+    const float *x_partials;
+    float w_unscale;               // 2^-k_w of the weight planes
 };
 
 // Role ablation for bottleneck experiments, compiled in only with -DSEGB_ROWS_ABLATION
@@ -199,7 +205,7 @@ struct RowsSmem {  // byte offsets from the 1024-aligned smem base
 __host__ __device__ inline RowsSmem rows_layout(const RowsParams &p, int ntaps, int kbc) {
     RowsSmem s;
     s.b = 0;
-    s.ring = s.b + ntaps * kbc * p.b_tile_bytes;
+    s.ring = s.b + ntaps * kbc * p.b_tile_bytes * (p.b_plane ? 2 : 1);  // F16: hi and lo weight planes
     s.bars = s.ring + p.ring * kbc * p.slot_bytes;
     s.total = s.bars + (1 + 2 * p.ring * kbc + 8) * 8 + 16;  // b_full, slots, 4 tfull + 4 tempty, TMEM addr
     return s;
@@ -239,9 +245,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // COSPLIT (with CG = 2, M = 128): the pair's B rows are [first channel halves | second halves],
 // so class c's accumulator is N/2 columns in both lane halves; otherwise (M = 256) B rows are
 // the group's (class, channel) list split in two and every CTA holds all N columns.
-template <int NH, int KBC, int SWAP, int MR, int RSEL, int CG = 1, bool COSPLIT = true>
+// F16: three MMAs per k-chunk on the scaled fp16 planes, hi*hi + hi*lo + lo*hi (the lo planes
+// AP16 / BP16 descriptor units after the hi ones), fp16 instruction descriptors.
+template <int NH, int KBC, int SWAP, int MR, int RSEL, int CG = 1, bool COSPLIT = true, bool F16 = false>
 __device__ __forceinline__ void issue_tile(uint32_t d0, uint32_t aLo0, uint32_t bLo0, uint32_t sq, uint32_t ring,
-                                           uint32_t S16, uint32_t B16, int N, uint32_t leader) {
+                                           uint32_t S16, uint32_t B16, int N, uint32_t leader, uint32_t AP16 = 0,
+                                           uint32_t BP16 = 0) {
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
     constexpr int CB = RSEL < 0 ? 0 : 2 * RSEL;  // first class held in this CTA's TMEM
     constexpr int DU = RSEL < 0 ? (SWAP ? NH : NH + 1) : NH;
@@ -265,11 +274,18 @@ __device__ __forceinline__ void issue_tile(uint32_t d0, uint32_t aLo0, uint32_t 
             const MmaGroup g = SCH.g[gi];
             const uint32_t a = arow[g.du] + kb * S16 + g.dc * 8;
             const uint32_t b = bLo0 + (kb * SCH.ntiles + g.b0) * B16;
-            const uint32_t idesc = idesc_bf16_m(MR * CG, g.nc * N);
+            const uint32_t idesc = F16 ? idesc_bf16_m(MR * CG, g.nc * N) & ~((1u << 7) | (1u << 10))  // fp16 x fp16
+                                       : idesc_bf16_m(MR * CG, g.nc * N);
+            const uint32_t d = d0 + (g.c0 - CB) * (COSPLIT ? N / CG : N);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-                tc_mma_lo<CG>(d0 + (g.c0 - CB) * (COSPLIT ? N / CG : N), a + kk * 2, b + kk * 2, idesc,
-                              (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u, leader);
+            for (int kk = 0; kk < 4; ++kk) {
+                tc_mma_lo<CG>(d, a + kk * 2, b + kk * 2, idesc, (SCH.fresh[gi] && kb == 0 && kk == 0) ? 0u : 1u,
+                              leader);
+                if constexpr (F16) {
+                    tc_mma_lo<CG>(d, a + kk * 2, b + BP16 + kk * 2, idesc, 1u, leader);
+                    tc_mma_lo<CG>(d, a + AP16 + kk * 2, b + kk * 2, idesc, 1u, leader);
+                }
+            }
         }
     }
 }
@@ -279,14 +295,17 @@ __device__ __forceinline__ void issue_tile(uint32_t d0, uint32_t aLo0, uint32_t 
 // the leader's barrier, which expects both halves)
 template <int NH, int KBC, int SWAP, int RSEL>
 __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB, uint64_t *bar, const RowsParams &prm,
-                                             int pair_rank = -1, bool cosplit = true) {
+                                             int pair_rank = -1, bool cosplit = true,
+                                             const CUtensorMap *tmBlo = nullptr) {
+    // tmBlo (F16): the lo plane's tiles go to the same offsets + prm.b_plane
     constexpr Schedule<NH, SWAP, RSEL> SCH = make_schedule<NH, SWAP, RSEL>();
+    const int planes = tmBlo ? 2 : 1;
     if (pair_rank >= 0 && !cosplit) {
         // M = 256 pairs: CTA r holds rows [r N/2, (r+1) N/2) of each group's (class, channel)
         // list, as half tiles: whole tiles of classes c0 + r nc/2 .. (nc >= 2) or the channel
         // half r of the single class (nc = 1); a group's halves start at half tile b0
         const uint32_t lb = mapa_rank(bar, 0);
-        if (pair_rank == 0) mbar_expect_tx(bar, 2 * SCH.ntiles * KBC * prm.b_tile_bytes);
+        if (pair_rank == 0) mbar_expect_tx(bar, 2 * planes * SCH.ntiles * KBC * prm.b_tile_bytes);
 #pragma unroll
         for (int gi = 0; gi < SCH.count; ++gi) {
             const MmaGroup g = SCH.g[gi];
@@ -297,32 +316,36 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
                 const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
                 const int tap = prm.cls[c].tap0 + u * NH + v;
                 for (int kb = 0; kb < KBC; ++kb)
-                    tma_load_3d_2sm(sB + (kb * SCH.ntiles + g.b0 + j) * prm.b_tile_bytes, tmB, lb, kb * 64, co_off,
-                                    tap);
+                    for (int pl = 0; pl < planes; ++pl)
+                        tma_load_3d_2sm(sB + pl * prm.b_plane + (kb * SCH.ntiles + g.b0 + j) * prm.b_tile_bytes,
+                                        pl ? tmBlo : tmB, lb, kb * 64, co_off, tap);
             }
         }
         return;
     }
     if (pair_rank >= 0) {
         const uint32_t lb = mapa_rank(bar, 0);
-        if (pair_rank == 0) mbar_expect_tx(bar, 2 * SCH.ntiles * KBC * prm.b_tile_bytes);
+        if (pair_rank == 0) mbar_expect_tx(bar, 2 * planes * SCH.ntiles * KBC * prm.b_tile_bytes);
 #pragma unroll
         for (int k = 0; k < SCH.ntiles; ++k) {
             const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
             const int tap = prm.cls[c].tap0 + u * NH + v;
             for (int kb = 0; kb < KBC; ++kb)
-                tma_load_3d_2sm(sB + (kb * SCH.ntiles + k) * prm.b_tile_bytes, tmB, lb, kb * 64,
-                                pair_rank * (prm.c_out / 2), tap);
+                for (int pl = 0; pl < planes; ++pl)
+                    tma_load_3d_2sm(sB + pl * prm.b_plane + (kb * SCH.ntiles + k) * prm.b_tile_bytes, pl ? tmBlo : tmB,
+                                    lb, kb * 64, pair_rank * (prm.c_out / 2), tap);
         }
         return;
     }
-    mbar_expect_tx(bar, SCH.ntiles * KBC * prm.b_tile_bytes);
+    mbar_expect_tx(bar, planes * SCH.ntiles * KBC * prm.b_tile_bytes);
 #pragma unroll
     for (int k = 0; k < SCH.ntiles; ++k) {
         const int c = SCH.btap[k] >> 8, u = (SCH.btap[k] >> 4) & 15, v = SCH.btap[k] & 15;
         const int tap = prm.cls[c].tap0 + u * NH + v;
         for (int kb = 0; kb < KBC; ++kb)
-            tma_load_3d(sB + (kb * SCH.ntiles + k) * prm.b_tile_bytes, tmB, bar, kb * 64, 0, tap);
+            for (int pl = 0; pl < planes; ++pl)
+                tma_load_3d(sB + pl * prm.b_plane + (kb * SCH.ntiles + k) * prm.b_tile_bytes, pl ? tmBlo : tmB, bar,
+                            kb * 64, 0, tap);
     }
 }
 
@@ -337,9 +360,12 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
 // the leader (rank 0) issues the MMAs; each CTA's TMEM gets its own MR positions with the first
 // channel half in lanes 0-63 and the second in lanes 64-127 (MR = 64), so all four epilogue
 // warps store full 32-lane rows.
-template <int NH, int KBC, int SWAP, int MR, int RS>
+// F16 (3xFP16): fp32 input rows are scaled, split into fp16 hi / lo planes by the loaders, the
+// MMA warp issues three MMAs per chunk and the epilogue writes fp32 times 2^-(k_x + k_w).
+template <int NH, int KBC, int SWAP, int MR, int RS, bool F16 = false>
 __global__ void __launch_bounds__(kRowsThreads, 1)
-    igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const RowsParams prm) {
+    igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
+                      const RowsParams prm) {
     constexpr bool TWO = RS == 3 || RS == 4;  // 2-SM pair: M = 128 (RS 3, MR 64) or 256 (RS 4, MR 128)
     constexpr bool COSPLIT = RS == 3;
     // RS = 5 (HALF): one CTA, every tile issued as two row-parity halves (schedules RSEL 0, 1)
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // 2i+1 run and the next tile's first half can start as soon as a half buffer is free
     constexpr bool HALF = RS == 5;
     constexpr int NCL = (RS == 2 || HALF) ? 2 : 4;  // parity classes per accumulator buffer
-    constexpr int NBUF = HALF ? 4 : 2;              // TMEM accumulator buffers
+    constexpr int NBUF = (HALF || F16) ? 4 : 2;     // TMEM accumulator buffers (F16: deeper, 64-position tiles)
     // M = 64 rows with two channel blocks: loader warps 0-1 fill block 0, warps 2-3 block 1 of
     // the same input row at once (else each unit is one (row, block) filled by all four)
     constexpr bool PAIRKB = MR == 64 && KBC == 2;
@@ -389,7 +415,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        if (F16) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmBlo) : "memory");
     }
+    const CUtensorMap *tmLo = F16 ? &tmBlo : nullptr;
     const uint32_t tcols = tmem_pow2(NBUF * NCL * N / (COSPLIT ? 2 : 1));  // buffers x NCL classes x N (RS 3: N/2)
     if (warp == 1) {
         if (TWO) {
@@ -421,8 +449,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #endif
         if (warp == 0) {
             if (lane == 0) {  // ---------------- the resident weights, in schedule order
-                if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank, COSPLIT);
-                else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm);
+                if (TWO) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, rank, COSPLIT, tmLo);
+                else if (RS == 1) load_weights<NH, KBC, SWAP, -1>(sB, &tmB, b_full, prm, -1, true, tmLo);
                 else if (HALF) {  // both row parities' schedules, the second after the first's tiles
                     load_weights<NH, KBC, SWAP, 0>(sB, &tmB, b_full, prm);
                     load_weights<NH, KBC, SWAP, 1>(sB + make_schedule<NH, SWAP, 0>().ntiles * KBC * prm.b_tile_bytes,
@@ -491,8 +519,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
                     }
                 } else if (ABL(4)) {
-                } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
-                else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
+                } else if (TWO) issue_tile<NH, KBC, SWAP, MR, -1, 2, COSPLIT, F16>(d0, aLo0, bLo0, sq, ring, S16, B16, N,
+                                                                                    leader, prm.slot_plane >> 4,
+                                                                                    prm.b_plane >> 4);
+                else if (RS == 1) issue_tile<NH, KBC, SWAP, MR, -1, 1, true, F16>(d0, aLo0, bLo0, sq, ring, S16, B16, N,
+                                                                                  leader, prm.slot_plane >> 4,
+                                                                                  prm.b_plane >> 4);
                 else if (rsel == 0) issue_tile<NH, KBC, SWAP, MR, 0>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
                 else issue_tile<NH, KBC, SWAP, MR, 1>(d0, aLo0, bLo0, sq, ring, S16, B16, N, leader);
                 // commits, branch-free like the MMAs (lane `leader` issues them)
@@ -518,7 +550,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (sq >= (uint32_t)ring) { sq -= ring; phq ^= 1; }
                 ri = ri_next;
                 __syncwarp();
-                if (!HALF && ++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (!HALF && ++acc == NBUF) { acc = 0; acc_phase ^= 1; }
             }
             }
         }  // warps 2, 3: idle (they only take part in warpgroup 0's register release)
@@ -539,8 +571,156 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const int th = PAIRKB ? tt & 63 : tt;             // index among the threads of one slot
         const int HL = -prm.dmin_c, HR = prm.slot_rows - MR - HL;
         const bool col_active = cc < MR / 8;  // MR = 64 (unpaired) uses half the column chunks
-        const __nv_bfloat16 *x = reinterpret_cast<const __nv_bfloat16 *>(prm.x);
         const int64_t plane_in = (int64_t)prm.h * prm.w;
+        // unit cursor (tile, row of its window, channel block)
+        auto advance = [&](int &ut, int &ul, int &ukb) {
+            if (++ukb == UKB) {
+                ukb = 0;
+                if (++ul == nr && ++ut < t1) ul = nr - loads_of(ut);
+            }
+        };
+        if constexpr (F16) {
+            // ---- 3xFP16: fp32 rows (8 channels x 8 columns per thread, 16-byte loads), scaled by
+            // 2^k_x, split into fp16 hi / lo, 8x8-transposed in registers into both slot planes
+            const float *xf = reinterpret_cast<const float *>(prm.x);
+            float mx = 0.f;
+            for (int i = lane; i < kAbsmaxBlocks; i += 32) mx = fmaxf(mx, __ldg(prm.x_partials + i));
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+            const float sc = ldexpf(1.f, f16_scale_exp(mx));
+            constexpr int KLB = 2;  // units in flight per thread (64 fp32 registers each)
+            auto load_unit = [&](int t, int l, int kb, float4 (&r)[16], float (&hv)[8]) {
+                t += toff;
+                const int i = t % prm.rows, rest = t / prm.rows;
+                const int ms = rest % prm.msub, b = rest / prm.msub;
+                const int row = i + dminr + l;
+                const int j0 = ms * MR;
+                const bool in_row = row >= 0 && row < prm.h;
+                const bool rok = in_row && col_active;
+                const int ch0 = (PAIRKB ? kbt : kb) * 64 + cg * 8;
+                const float *src = xf + ((int64_t)b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    r[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    r[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (rok && ch0 + c < prm.c_in) {
+                        const float4 *p4 = reinterpret_cast<const float4 *>(src + (int64_t)c * plane_in + cc * 8);
+                        r[2 * c] = __ldg(p4);
+                        r[2 * c + 1] = __ldg(p4 + 1);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) hv[c] = 0.f;
+                if (th < (HL + HR) * 8) {  // halo column tasks: (halo col, channel group)
+                    const int hc = th >> 3;
+                    const int col = hc < HL ? j0 - HL + hc : j0 + MR + (hc - HL);
+                    if (in_row && col >= 0 && col < prm.w) {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            if (ch0 + c < prm.c_in) hv[c] = __ldg(src + (int64_t)c * plane_in + (col - j0));
+                    }
+                }
+            };
+            float4 rb[KLB][16];
+            float hb[KLB][8];
+            int bkb[KLB];
+            bool bv[KLB];
+            int ct = t0, cl = t0 < t1 ? nr - loads_of(t0) : 0, ckb_ = 0;
+#pragma unroll
+            for (int k = 0; k < KLB; ++k) {
+                bv[k] = ct < t1;
+                bkb[k] = ckb_;
+                if (bv[k]) {
+                    load_unit(ct, cl, ckb_, rb[k], hb[k]);
+                    advance(ct, cl, ckb_);
+                }
+            }
+            uint32_t qs = 0, qph = 0;
+            bool more = bv[0];
+            while (more) {
+#pragma unroll
+                for (int k = 0; k < KLB; ++k) {
+                    if (!bv[k]) {
+                        more = false;
+                        break;
+                    }
+                    const int ckb = PAIRKB ? kbt : bkb[k];
+                    const int sidx = qs * KBC + ckb;
+                    if (!(ABL(64))) mbar_wait(&slot_empty[sidx], qph ^ 1);
+                    const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
+                    if (col_active && !(ABL(16))) {
+                        uint32_t hp[8][4], lp[8][4];  // [channel][k]: columns 2k, 2k+1 as fp16 pairs
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const float v[8] = {rb[k][2 * c].x, rb[k][2 * c].y, rb[k][2 * c].z, rb[k][2 * c].w,
+                                                rb[k][2 * c + 1].x, rb[k][2 * c + 1].y, rb[k][2 * c + 1].z,
+                                                rb[k][2 * c + 1].w};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                __half h0, l0, h1, l1;
+                                split_f16(v[2 * q] * sc, h0, l0);
+                                split_f16(v[2 * q + 1] * sc, h1, l1);
+                                hp[c][q] = pack_h2(h0, h1);
+                                lp[c][q] = pack_h2(l0, l1);
+                            }
+                        }
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) {
+                            uint32_t oh[4], ol[4];
+                            const uint32_t sel = (w & 1) ? 0x7632 : 0x5410;
+#pragma unroll
+                            for (int m4 = 0; m4 < 4; ++m4) {
+                                oh[m4] = __byte_perm(hp[2 * m4][w >> 1], hp[2 * m4 + 1][w >> 1], sel);
+                                ol[m4] = __byte_perm(lp[2 * m4][w >> 1], lp[2 * m4 + 1][w >> 1], sel);
+                            }
+                            const int rho = HL + cc * 8 + w;
+                            const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(oh[0]),
+                                         "r"(oh[1]), "r"(oh[2]), "r"(oh[3])
+                                         : "memory");
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr + prm.slot_plane),
+                                         "r"(ol[0]), "r"(ol[1]), "r"(ol[2]), "r"(ol[3])
+                                         : "memory");
+                        }
+                    }
+                    if (th < (HL + HR) * 8) {
+                        const int hc = th >> 3;
+                        const int rho = hc < HL ? hc : HL + MR + (hc - HL);
+                        const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
+                        uint32_t oh[4], ol[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            __half h0, l0, h1, l1;
+                            split_f16(hb[k][2 * q] * sc, h0, l0);
+                            split_f16(hb[k][2 * q + 1] * sc, h1, l1);
+                            oh[q] = pack_h2(h0, h1);
+                            ol[q] = pack_h2(l0, l1);
+                        }
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(oh[0]), "r"(oh[1]),
+                                     "r"(oh[2]), "r"(oh[3])
+                                     : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr + prm.slot_plane),
+                                     "r"(ol[0]), "r"(ol[1]), "r"(ol[2]), "r"(ol[3])
+                                     : "memory");
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !(ABL(64))) {
+                        if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));
+                        else mbar_arrive(&slot_full[sidx]);
+                    }
+                    if (PAIRKB || ckb == KBC - 1) {
+                        if (++qs == (uint32_t)ring) { qs = 0; qph ^= 1; }
+                    }
+                    bv[k] = ct < t1;
+                    bkb[k] = ckb_;
+                    if (bv[k]) {
+                        load_unit(ct, cl, ckb_, rb[k], hb[k]);
+                        advance(ct, cl, ckb_);
+                    }
+                }
+            }
+        } else {
+        const __nv_bfloat16 *x = reinterpret_cast<const __nv_bfloat16 *>(prm.x);
         auto load_unit = [&](int t, int l, int kb, uint4 (&r)[8], uint4 &hv) {
             t += toff;
             const int i = t % prm.rows, rest = t / prm.rows;
@@ -572,13 +752,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     hv = make_uint4(h16[0] | (h16[1] << 16), h16[2] | (h16[3] << 16), h16[4] | (h16[5] << 16),
                                     h16[6] | (h16[7] << 16));
                 }
-            }
-        };
-        // unit cursor (tile, row of its window, channel block)
-        auto advance = [&](int &ut, int &ul, int &ukb) {
-            if (++ukb == UKB) {
-                ukb = 0;
-                if (++ul == nr && ++ut < t1) ul = nr - loads_of(ut);
             }
         };
         // kLoadBufs register buffers in rotation, the loop unrolled by as many so that no buffer
@@ -657,6 +830,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
             }
         }
+        }
     } else {
         // ---------------- epilogue (warps 4..7): warp reads TMEM lane quarter warp % 4. The
         // classes of a position are in registers, so each lane writes the pair of output
@@ -673,8 +847,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const int chalf = COSPLIT ? (quarter >> 1) : 0;  // this warp's output-channel half
         const int NEW = NE, cw0 = 0;  // channels per class this warp stores, its first one
         auto release_acc = [&](int a) {
+#ifdef SEGB_ROWS_RELAXED_ARRIVE  // measured 3% slower on l7 fp32, no change on bf16 l6/l7
+            if (TWO) mbar_arrive_relaxed_cluster(mapa_rank(&tempty[a], 0));
+            else mbar_arrive_relaxed(&tempty[a]);
+#else
             if (TWO) mbar_arrive_cluster(mapa_rank(&tempty[a], 0));
             else mbar_arrive(&tempty[a]);
+#endif
         };
         // With even P the classes with row/column parity 0 fill output row 2i and the even
         // columns; with odd P (SWAP) it is the parity-1 classes (engines.py:338-347).
@@ -685,6 +864,61 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         constexpr int HT = HALF ? 2 : 1;  // accumulator buffers (half tiles) per tile
+        if constexpr (F16) {
+            // ---- 3xFP16: fp32 output. A lane holds the four classes of its position, i.e. output
+            // columns (2j, 2j+1) of rows 2i and 2i+1: one 8-byte store per row and channel (a warp
+            // instruction writes 256 contiguous bytes), times 2^-(k_x + k_w) (exact).
+            static_assert(NCL == 4, "3xFP16 rows: all four classes per accumulator buffer");
+            float mx = 0.f;
+            for (int q = lane; q < kAbsmaxBlocks; q += 32) mx = fmaxf(mx, __ldg(prm.x_partials + q));
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+            const float us = ldexpf(1.f, -f16_scale_exp(mx)) * prm.w_unscale;
+            const int64_t plane = (int64_t)prm.oh * prm.ow;
+            constexpr int C00 = class_slot(2 * RE + SE), C01 = class_slot(2 * RE + (1 - SE));
+            constexpr int C10 = class_slot(2 * (1 - RE) + SE), C11 = class_slot(2 * (1 - RE) + (1 - SE));
+            for (int t = t0; t < t1; ++t) {
+                const int ta = t + toff;
+                const int i = ta % prm.rows, rest = ta / prm.rows;
+                const int ms = rest % prm.msub, b = rest / prm.msub;
+                if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
+                float *pf = reinterpret_cast<float *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE) * plane +
+                            (int64_t)(2 * i + row_off) * prm.ow + (int64_t)ms * 2 * MR + 2 * m;
+                constexpr int CH = kEpiChunk;
+                uint32_t v[NCL][CH], v2[NCL][CH];
+#pragma unroll
+                for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE, v[c]);
+                auto chunk = [&](int co0, uint32_t (&cur)[NCL][CH], uint32_t (&nxt)[NCL][CH]) {
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < NCL; ++c) reg_fence_chunk(cur[c]);
+                    if (co0 + CH < NE) {
+#pragma unroll
+                        for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE + co0 + CH, nxt[c]);
+                    } else {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) release_acc(acc);
+                    }
+#pragma unroll
+                    for (int k = 0; k < CH; ++k) {
+                        const float2 r0 = make_float2(__uint_as_float(cur[C00][k]) * us, __uint_as_float(cur[C01][k]) * us);
+                        const float2 r1 = make_float2(__uint_as_float(cur[C10][k]) * us, __uint_as_float(cur[C11][k]) * us);
+                        if (lane_active && !(ABL(1))) {
+                            float *q = pf + (int64_t)(co0 + k) * plane;
+                            *reinterpret_cast<float2 *>(q) = r0;
+                            *reinterpret_cast<float2 *>(q + prm.ow) = r1;
+                        }
+                    }
+                };
+                for (int co0 = 0; co0 < NE; co0 += 2 * CH) {
+                    chunk(co0, v, v2);
+                    if (co0 + CH < NE) chunk(co0 + CH, v2, v);
+                }
+                if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+            }
+        } else
         for (int u = t0 * HT; u < t1 * HT; ++u) {
             const int t = u / HT;
             const int ta = t + toff;
@@ -787,9 +1021,18 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
+static bool rows_f16(const IgemmShape &s) { return s.compute == SEGB_F32 && s.f16x3; }
+
 static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc, int &swap, int &mr, int &nsplit) {
-    if (s.n % 2 != 0 || s.n > 6 || s.x_dtype != SEGB_BF16) return false;
-    if (s.y_dtype != SEGB_BF16) return false;  // fp32 output takes K3
+    const bool f16 = rows_f16(s);
+    if (f16) {  // 3xFP16: fp32 in / out, one channel block, the 2-SM pair over batch halves
+        if (s.x_dtype != SEGB_F32 || s.y_dtype != SEGB_F32) return false;
+        if (s.n != 4 || s.c_in > 64 || s.c_in % 8 != 0 || s.batch % 2 != 0 || s.c_out % 32 != 0) return false;
+    } else if (s.compute != SEGB_BF16) {
+        return false;
+    }
+    if (s.n % 2 != 0 || s.n > 6 || (!f16 && s.x_dtype != SEGB_BF16)) return false;
+    if (!f16 && s.y_dtype != SEGB_BF16) return false;  // fp32 output takes K3
     if (s.c_out < 16 || s.c_out > 64 || s.c_out % 16 != 0) return false;
     if (s.w % 8 != 0 || s.w < 64) return false;
     const int oh = 2 * s.h + 2 * s.pad - s.n, ow = 2 * s.w + 2 * s.pad - s.n;
@@ -813,7 +1056,9 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
         dmax_c = std::max(dmax_c, g.base_s + nh - 1 - p);
     }
     const int rows = oh / 2, cols = ow / 2;
-    if (cols % 128 == 0) mr = 128;
+    if (f16 && cols % 64 != 0) return false;
+    if (f16) mr = 64;  // M = 128 pair MMAs over 64-wide tiles: half the weights per CTA
+    else if (cols % 128 == 0) mr = 128;
     else if (cols % 64 == 0) mr = 64;  // M=64 MMAs (half rate, but every input row loaded once)
     else return false;
     prm.c_in = s.c_in; prm.h = s.h; prm.w = s.w;
@@ -826,6 +1071,11 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     kbc = (s.c_in + 63) / 64;
     if (kbc > 2) return false;
     prm.slot_bytes = (prm.slot_rows * 128 + 1023) / 1024 * 1024;
+    prm.slot_plane = prm.b_plane = 0;
+    if (f16) {  // hi plane then lo plane per slot (1024-aligned: the same swizzle phase)
+        prm.slot_plane = prm.slot_bytes;
+        prm.slot_bytes *= 2;
+    }
     const int64_t total = s.batch * (int64_t)prm.msub * rows;
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
@@ -837,10 +1087,11 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     // 128-wide class grids (nsplit = 4, RS = 4) can likewise pair into M=256 MMAs (half the
     // weights' shared memory, a deeper row ring, half the B operand reads per SM); measured
     // slower on ebgan_l7 (0.70 vs 0.64 ms), so only with SEGB200_ROWS_PAIR=4.
-    const bool pair_ok = s.batch % 2 == 0 && s.c_out % 32 == 0 && nh == 2 && !(pe && !atoi(pe));
+    const bool pair_ok = s.batch % 2 == 0 && s.c_out % 32 == 0 && nh == 2 && (f16 || !(pe && !atoi(pe)));
     const bool pair128 = pe && atoi(pe) == 4;
     if (pair_ok && (mr == 64 || pair128)) {
         prm.b_tile_bytes = s.c_out / 2 * 128;
+        if (f16) prm.b_plane = 4 * nh * nh * kbc * prm.b_tile_bytes;
         prm.half_tiles = prm.total_tiles / 2;
         for (prm.ring = kRingMax; prm.ring > std::max(4, prm.nr); --prm.ring)
             if (rows_layout(prm, 4 * nh * nh, kbc).total + 1024 <= 227 * 1024) break;
@@ -849,6 +1100,7 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
             return true;
         }
     }
+    if (f16) return false;
     prm.b_tile_bytes = s.c_out * 128;
     // all four classes per CTA if their weights fit next to the row ring, else split the
     // classes over a CTA pair by row parity (half the weights each)
@@ -870,7 +1122,9 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
 }
 
 // the (NH, KBC, SWAP, MR, NS) variants compiled below
-static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit) {
+static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit, bool f16 = false) {
+    // (odd P with w % 8 == 0 never gives a 64-multiple class grid for n = 4: no SWAP variant)
+    if (f16) return nh == 2 && kbc == 1 && mr == 64 && nsplit == 3 && swap == 0;
     if (nsplit == 3) return mr == 64 && nh == 2;
     if (nsplit == 4) return mr == 128 && nh == 2;
     if (mr == 128 && nsplit == 1) return true;
@@ -883,16 +1137,17 @@ static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit) {
 bool igemm_rows_supported(const IgemmShape &s) {
     RowsParams prm;
     int nh, kbc, swap, mr, nsplit;
-    return rows_params(s, prm, nh, kbc, swap, mr, nsplit) && rows_instantiated(nh, kbc, swap, mr, nsplit) &&
-           tensor_map_encoder() != nullptr;
+    return rows_params(s, prm, nh, kbc, swap, mr, nsplit) &&
+           rows_instantiated(nh, kbc, swap, mr, nsplit, rows_f16(s)) && tensor_map_encoder() != nullptr;
 }
 
-template <int NH, int KBC, int SWAP, int MR, int NS>
-static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const RowsParams &prm) {
-    auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS>;
+template <int NH, int KBC, int SWAP, int MR, int NS, bool F16 = false>
+static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const CUtensorMap &tmBlo,
+                        const RowsParams &prm) {
+    auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS, F16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (NS < 3 || NS == 5) {
-        kern<<<grid, kRowsThreads, smem, st>>>(tmB, prm);
+        kern<<<grid, kRowsThreads, smem, st>>>(tmB, tmBlo, prm);
         return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -907,25 +1162,46 @@ static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, tmB, prm);
+    cudaLaunchKernelEx(&cfg, kern, tmB, tmBlo, prm);
 }
 
-int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, cudaStream_t st) {
+int64_t igemm_rows_workspace_bytes(const IgemmShape &s) { return rows_f16(s) ? 1024 : 0; }
+
+int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,
+                   int64_t ws_bytes, cudaStream_t st) {
+    const bool f16 = rows_f16(s);
     RowsParams prm;
     int nh, kbc, swap, mr, nsplit;
     if (!rows_params(s, prm, nh, kbc, swap, mr, nsplit))
         return fail(SEGB_ERR_UNSUPPORTED, "row-streaming implicit GEMM: unsupported shape");
     auto encode = tensor_map_encoder();
-    CUtensorMap tmB;
+    CUtensorMap tmB, tmBlo;
     {
         cuuint64_t dims[3] = {(cuuint64_t)s.c_in_pad, (cuuint64_t)s.c_out_pad, (cuuint64_t)s.n * s.n};
         cuuint64_t strides[2] = {(cuuint64_t)s.c_in_pad * 2, (cuuint64_t)s.c_out_pad * s.c_in_pad * 2};
         cuuint32_t box[3] = {64, (cuuint32_t)((nsplit == 3 || nsplit == 4) ? s.c_out / 2 : s.c_out), 1};
         cuuint32_t es[3] = {1, 1, 1};
-        CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(wg), dims, strides, box, es,
+        const CUtensorMapDataType dt = f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        CUresult r = encode(&tmB, dt, 3, const_cast<void *>(wg), dims, strides, box, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (weights): error %d", (int)r);
+        tmBlo = tmB;
+        if (f16) {
+            r = encode(&tmBlo, dt, 3, const_cast<void *>(wg_lo), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(SEGB_ERR_CUDA, "tensor map (weights lo): error %d", (int)r);
+        }
+    }
+    prm.x_partials = nullptr;
+    prm.w_unscale = ldexpf(1.f, -s.w_exp);
+    if (f16) {  // the input's scale: absmax partials into the caller's workspace
+        if (!ws || ws_bytes < igemm_rows_workspace_bytes(s))
+            return fail(SEGB_ERR_VALUE, "row-streaming GEMM: workspace of %lld bytes needed, got %lld",
+                        (long long)igemm_rows_workspace_bytes(s), (long long)ws_bytes);
+        float *partials = (float *)ws;
+        if (int rc = run_absmax_partials(x, SEGB_F32, s.batch * (int64_t)s.c_in * s.h * s.w, partials, st)) return rc;
+        prm.x_partials = partials;
     }
     prm.x = x;
     prm.y = y;
@@ -962,8 +1238,12 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, void *y, 
     }
     int rc = SEGB_OK;
 #define SEGB_ROWS_CASE(NH_, KBC_, SW_, MR_, NS_)                                                  \
-    if (nh == NH_ && kbc == KBC_ && swap == SW_ && mr == MR_ && nsplit == NS_)                     \
-        launch_rows<NH_, KBC_, SW_, MR_, NS_>(grid, smem, st, tmB, prm);                           \
+    if (!f16 && nh == NH_ && kbc == KBC_ && swap == SW_ && mr == MR_ && nsplit == NS_)             \
+        launch_rows<NH_, KBC_, SW_, MR_, NS_>(grid, smem, st, tmB, tmBlo, prm);                    \
+    else
+    // 3xFP16 (fp32 in / out): EB-GAN l7's shape family
+    if (f16 && nh == 2 && kbc == 1 && swap == 0 && mr == 64 && nsplit == 3)
+        launch_rows<2, 1, 0, 64, 3, true>(grid, smem, st, tmB, tmBlo, prm);
     else
     // instantiated: n in {2, 4, 6} x channel blocks x P parity for 128-wide rows; the n = 4
     // (GAN) family also for 64-wide rows and with the row-parity split

@@ -686,7 +686,8 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
 
 static bool use_rows(const IgemmShape &s) {
     const char *e = getenv("SEGB200_IGEMM_GENERIC");
-    return s.compute == SEGB_BF16 && !(e && atoi(e)) && igemm_rows_supported(s);
+    return (s.compute == SEGB_BF16 || (s.compute == SEGB_F32 && s.f16x3)) && !(e && atoi(e)) &&
+           igemm_rows_supported(s);
 }
 
 bool igemm_supported(const IgemmShape &s) {
@@ -696,7 +697,7 @@ bool igemm_supported(const IgemmShape &s) {
 
 const char *igemm_kernel_name(const IgemmShape &s) {
     if (igemm_scatter_supported(s)) return "K3c scatter-GEMM + gather (bf16)";
-    if (use_rows(s)) return "K3b row-streaming GEMM (bf16)";
+    if (use_rows(s)) return s.compute == SEGB_F32 ? "K3b row-streaming GEMM (3xFP16)" : "K3b row-streaming GEMM (bf16)";
     const int mode = fp32_mode(s);
     if (mode == kModeF16x3) return "K3 implicit GEMM (3xFP16)";
     if (mode == kModeTf32x3) return "K3 implicit GEMM (3xTF32)";
@@ -709,7 +710,7 @@ const char *igemm_kernel_name(const IgemmShape &s) {
 // none from here (K3c's tap products are counted by igemm_scatter_workspace_bytes).
 int64_t igemm_workspace_bytes(const IgemmShape &s) {
     if (igemm_scatter_supported(s)) return igemm_scatter_workspace_bytes(s);
-    if (use_rows(s)) return 0;
+    if (use_rows(s)) return igemm_rows_workspace_bytes(s);
     const int mode = fp32_mode(s);
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
     const int64_t bpe = mode == kModeTf32x3 ? 8 : (mode == kModeF16x3 ? 4 : 2);  // bytes per element, all planes
@@ -752,7 +753,7 @@ static int launch_k3(unsigned grid, size_t smem, cudaStream_t st, const CUtensor
 
 int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,
               int64_t ws_bytes, cudaStream_t st) {
-    if (use_rows(s)) return run_igemm_rows(s, x, wg, y, st);
+    if (use_rows(s)) return run_igemm_rows(s, x, wg, wg_lo, y, ws, ws_bytes, st);
     IgemmParams prm;
     if (!make_params(s, prm)) return fail(SEGB_ERR_UNSUPPORTED, "implicit GEMM: unsupported shape");
     if (!tensor_map_encoder()) return fail(SEGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");

@@ -100,6 +100,15 @@ __device__ __forceinline__ uint32_t mapa_rank(const void *p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// relaxed arrivals: hand back a resource whose last use was a tcgen05.ld already waited for
+// (tcgen05.wait::ld + tcgen05.fence::before_thread_sync), so no memory data has to be published --
+// a release would also wait for the thread's preceding global stores to drain
+__device__ __forceinline__ void mbar_arrive_relaxed_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // TMA loads for a CTA pair (cta_group::2): data into this CTA's shared memory, complete_tx on
 // the mbarrier at shared::cluster address `bar` (the leader CTA's)
 __device__ __forceinline__ void tma_load_4d_2sm(void *dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,

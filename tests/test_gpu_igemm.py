@@ -350,3 +350,33 @@ def test_3xfp16_nan_propagates():
     assert np.array_equal(np.isnan(y), np.isnan(ref))
     fin = ~np.isnan(ref)
     assert O.compare(y[fin], ref[fin], 1e-5, 1e-6)["passed"]
+
+
+ROWS_F16_CASES = [  # K3b row-streaming 3xFP16 (fp32 in / out): 2-SM pairs over batch halves
+    ("ebgan_l7_b2", 128, 128, 64, 4, 64, 2, 2),
+    ("w64_b4", 32, 64, 64, 4, 64, 2, 4),
+    ("c_out32", 16, 64, 64, 4, 32, 2, 2),
+    ("h4_b2", 4, 64, 64, 4, 64, 2, 2),
+    ("b6_h8", 8, 128, 64, 4, 64, 2, 6),
+]
+
+
+@pytest.mark.parametrize("name,h,w,ci,n,co,pad,b", ROWS_F16_CASES)
+def test_rows_3xfp16_fp32_gate(monkeypatch, name, h, w, ci, n, co, pad, b):
+    """fp32 layers on the row-streaming kernel (3xFP16) meet the reference's fp32 gate, and agree
+    with the generic K3 3xFP16 kernel (SEGB200_IGEMM_GENERIC=1) to the same gate"""
+    import torch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    x = device_unit_floats((b, ci, h, w), 700 + ci, dtype=torch.float32)
+    bank = O.gen_kernel_bank(ci, co, n, 701 + ci)
+    layer = P.prepare_layer(bank, pad)
+    kern = layer.describe_path(b, h, w)
+    assert "K3b" in kern and "3xFP16" in kern, (name, kern)
+    y = layer.forward(x).cpu().numpy()
+    ref = O.forward_segregated_batch(x.cpu().numpy().astype(np.float64), bank.astype(np.float64), pad)
+    rep = O.compare(y, ref, 1e-5, 1e-6)
+    assert rep["passed"], (name, rep)
+    monkeypatch.setenv("SEGB200_IGEMM_GENERIC", "1")
+    assert "K3 implicit GEMM (3xFP16)" in layer.describe_path(b, h, w)
+    yg = layer.forward(x).cpu().numpy()
+    assert O.compare(y, yg.astype(np.float64), 1e-5, 1e-6)["passed"], name
