@@ -57,7 +57,15 @@ enum segb_status {
     SEGB_ERR_UNSUPPORTED = 5
 };
 
-enum segb_dtype { SEGB_F32 = 0, SEGB_F64 = 1, SEGB_BF16 = 2 };
+enum segb_dtype {
+    SEGB_F32 = 0,
+    SEGB_F64 = 1,
+    SEGB_BF16 = 2,
+    /* x only: the interleaved u8 image payload (batch, in_h, in_w, c_in) of binary P6 PPMs,
+     * decoded in the direct kernel's loads as float32(u8) / 255 with IEEE division -- bitwise
+     * the reference's parse_ppm values (tensor_io.py:27-52); fp32 compute, f32 y */
+    SEGB_U8_HWC = 3
+};
 
 /* engines.py:44-46 ENGINE_REFERENCE / ENGINE_SEGREGATED */
 enum segb_engine { SEGB_ENGINE_REFERENCE = 0, SEGB_ENGINE_SEGREGATED = 1 };

@@ -146,3 +146,47 @@ def route(segconv) -> None:
     for mod in (engines, segconv):
         mod.transpose_conv_reference_counted = transpose_conv_reference_counted
         mod.transpose_conv_segregated_counted = transpose_conv_segregated_counted
+
+
+# ------------------------------------------------------------------ GPU columns for the harness
+
+def gpu_record(config, seed: int, index: int, batch: int = 64, compute: str = "fp32", repeats: int = 10) -> dict:
+    """The "gpu" object the routed harness adds to a reference layer record:
+    the layer on a device-resident batch of `batch` samples of the harness's input stream (sample 0
+    is the reference's own input, bench.py:299-301), CUDA-event timed (median of `repeats`), with the
+    kernel the dispatcher picked and useful GMAC/s (mult_count_segregated x batch / time)."""
+    import torch
+
+    import paper_2502_20493_b200 as P
+    from paper_2502_20493_b200.synth import device_unit_floats, harness_seeds
+    in_seed, bank_seed = harness_seeds(seed, index)
+    dt = torch.bfloat16 if compute == "bf16" else torch.float32
+    bank = device_unit_floats((config.c_in, config.c_out, config.kernel_n, config.kernel_n), bank_seed)
+    layer = P.prepare_layer(bank, config.pad, compute=compute)
+    x = device_unit_floats((batch, config.c_in, config.input_h, config.input_w), in_seed, dtype=dt)
+    y = layer.forward(x)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(repeats)]
+    for a, b in ev:
+        a.record()
+        layer.forward(x, out=y)
+        b.record()
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in ev)[repeats // 2]
+    macs = P.mult_count_segregated(P.TransposeConvSpec(config.input_h, config.input_w, config.kernel_n,
+                                                       config.pad, config.c_in, config.c_out)) * batch
+    return {"device": torch.cuda.get_device_name(), "batch": batch, "compute": compute,
+            "kernel": layer.describe_path(batch, config.input_h, config.input_w), "time_s": ms * 1e-3,
+            "useful_gmacs": macs / (ms * 1e-3) / 1e9}
+
+
+def run_benchmark_gpu(segconv, configs, options=None, batch: int = 64, compute: str = "fp32"):
+    """segconv.bench.run_benchmark with the segregated engine on the GPU (route()), plus a "gpu"
+    object per layer record; the reference's report schema otherwise unchanged (emit_report, the
+    CLI and the service consume it as is)."""
+    route(segconv)
+    options = options or segconv.bench.RunOptions()
+    report = segconv.bench.run_benchmark(list(configs), options)
+    for index, (config, rec) in enumerate(zip(configs, report.layers)):
+        if rec.get("error") is None:
+            rec["gpu"] = gpu_record(config, options.seed, index, batch, compute)
+    return report

@@ -24,7 +24,7 @@ from .engines import (
 from .errors import ShapeError, SpecError
 from .segregation import SubKernelSet, merge_subkernels, segregate_kernel
 from .stack import PreparedStack, prepare_stack
-from . import harness, tensor_io  # noqa: E402
+from . import tensor_io  # noqa: E402
 from .spec import (
     EffectivePadding,
     TransposeConvSpec,

@@ -367,7 +367,16 @@ static int plan_forward(const segb_layer *L, int x_dtype, int64_t batch, int in_
     if (batch < 1) return fail(SEGB_ERR_SHAPE, "batch must be >= 1, got %lld", (long long)batch);
     if (int rc = check_spec(in_h, in_w, L->n, L->pad, L->c_in, L->c_out, &pl.oh, &pl.ow)) return rc;
     if (compute < 0) compute = L->compute;
-    if (!valid_dtype(compute) || !valid_dtype(x_dtype) || !valid_dtype(y_dtype))
+    if (x_dtype == SEGB_U8_HWC) {  // the fused dataset-image path: K2, fp32
+        if (compute != SEGB_F32 || y_dtype != SEGB_F32)
+            return fail(SEGB_ERR_VALUE, "u8 image input computes in fp32 into f32 y (compute %d, y %d)", compute,
+                        y_dtype);
+        if (path == SEGB_PATH_IGEMM) return fail(SEGB_ERR_UNSUPPORTED, "u8 image input runs on the direct kernel");
+        path = SEGB_PATH_DIRECT;
+    } else if (!valid_dtype(x_dtype)) {
+        return fail(SEGB_ERR_VALUE, "unknown x dtype %d", x_dtype);
+    }
+    if (!valid_dtype(compute) || !valid_dtype(y_dtype))
         return fail(SEGB_ERR_VALUE, "unknown dtype (x %d, y %d, compute %d)", x_dtype, y_dtype, compute);
     if (path == SEGB_PATH_AUTO)
         path = igemm_ok(L, x_dtype, batch, in_h, in_w, compute, y_dtype) ? SEGB_PATH_IGEMM : SEGB_PATH_DIRECT;
@@ -431,6 +440,7 @@ static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch
     a.nqc = (ow - 1 + a.swap) / 2 + 1;
     const bool ref = L->engine == SEGB_ENGINE_REFERENCE;
     if (ref) a.p = L->pad;  // the reference engine pads the upsampled map by P
+    if (x_dtype == SEGB_U8_HWC) return launch_direct_u8(a, ref, st);
     switch (compute) {
         case SEGB_F32:
             if (x_dtype != SEGB_F32 || y_dtype != SEGB_F32)
@@ -450,6 +460,7 @@ int segb_describe_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h
     if (int rc = plan_forward(L, x_dtype, batch, in_h, in_w, y_dtype, compute, path, pl)) return rc;
     const char *name = "K2 direct (fp32 FFMA)";
     if (pl.path == SEGB_PATH_IGEMM) name = igemm_kernel_name(pl.s);
+    else if (x_dtype == SEGB_U8_HWC) name = "K2 direct (u8 image decoded on load, fp32 FFMA)";
     else if (pl.compute == SEGB_F64) name = "K2 direct (fp64)";
     else if (pl.compute == SEGB_BF16) name = "K2 direct (bf16 operands, fp32 FFMA)";
     if (buf && buf_len > 0) snprintf(buf, (size_t)buf_len, "%s", name);

@@ -53,6 +53,19 @@ template <> __device__ __forceinline__ float load_x<__nv_bfloat16, float, false>
     return __bfloat162float(*p);
 }
 template <> __device__ __forceinline__ double load_x<double, double, false>(const double *p) { return __ldg(p); }
+// dataset images: the interleaved u8 PPM payload read in place, decoded on load
+// exactly as the reference decodes it, float32(u8) / float32(255) with IEEE division
+// (tensor_io.py:52), so the fused path computes on the very values parse_ppm produces
+template <> __device__ __forceinline__ float load_x<uint8_t, float, false>(const uint8_t *p) {
+    return __fdiv_rn((float)__ldg(p), 255.0f);
+}
+
+// Input addressing: NCHW for float inputs; a uint8_t input is the interleaved (B, H, W, C) image
+// payload (channel stride 1, column stride C).
+template <typename TX> struct XLayout {
+    static constexpr bool HWC = sizeof(TX) == 1;
+    __device__ __forceinline__ static int64_t chan(int64_t plane) { return HWC ? 1 : plane; }
+};
 
 template <typename TY, typename TC> __device__ __forceinline__ void store_y(TY *p, TC v);
 template <> __device__ __forceinline__ void store_y<float, float>(float *p, float v) { *p = v; }
@@ -122,6 +135,10 @@ __global__ void __launch_bounds__(128, (COB <= 2 && sizeof(TC) == 4) ? 6 : 1) di
     const TX *xb = reinterpret_cast<const TX *>(a.x) + b * a.c_in * plane;
     const TC *wsrc = reinterpret_cast<const TC *>(a.w);
     const int tid = threadIdx.y * 32 + threadIdx.x;
+    constexpr bool HWC = XLayout<TX>::HWC;
+    const int es = HWC ? a.c_in : 1;                  // column (element) stride
+    const int64_t rs = (int64_t)a.w_in * es;          // row stride
+    const int64_t cs = XLayout<TX>::chan(plane);      // channel stride
 
     TC acc[COB][2 * RQ][2 * CQ];
 #pragma unroll
@@ -139,23 +156,24 @@ __global__ void __launch_bounds__(128, (COB <= 2 && sizeof(TC) == 4) ? 6 : 1) di
     for (int i = 0; i < WR; ++i) rok[i] = (unsigned)(row0 + i) < (unsigned)a.h;
 #pragma unroll
     for (int j = 0; j < WC; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
-    const TX *xw = xb + (int64_t)row0 * a.w_in + col0;  // window origin of channel 0 (may point outside)
+    const TX *xw = xb + (int64_t)row0 * rs + (int64_t)col0 * es;  // window origin of channel 0 (may point outside)
 
     auto load_win = [&](TC (&dst)[WR][WC], int ci_abs) {
-        const TX *xc = xw + (int64_t)ci_abs * plane;
-        if (warp_inside) {  // one row pointer per window row, immediate column offsets
+        const TX *xc = xw + (int64_t)ci_abs * cs;
+        if (warp_inside) {  // one row pointer per window row, immediate column offsets (NCHW)
 #pragma unroll
             for (int i = 0; i < WR; ++i) {
-                const TX *rp = xc + i * a.w_in;
+                const TX *rp = xc + i * rs;
 #pragma unroll
-                for (int j = 0; j < WC; ++j) dst[i][j] = load_x<TX, TC, RBF>(rp + j);
+                for (int j = 0; j < WC; ++j) dst[i][j] = load_x<TX, TC, RBF>(rp + j * es);
             }
         } else {
 #pragma unroll
             for (int i = 0; i < WR; ++i) {
-                const TX *rp = xc + i * a.w_in;
+                const TX *rp = xc + i * rs;
 #pragma unroll
-                for (int j = 0; j < WC; ++j) dst[i][j] = (rok[i] && cok[j]) ? load_x<TX, TC, RBF>(rp + j) : TC(0);
+                for (int j = 0; j < WC; ++j)
+                    dst[i][j] = (rok[i] && cok[j]) ? load_x<TX, TC, RBF>(rp + j * es) : TC(0);
             }
         }
     };
@@ -283,8 +301,10 @@ __global__ void __launch_bounds__(256) direct_generic_kernel(DirectArgs a) {
         const int bx = (xo + r) / 2 - a.p, by = (yo + s) / 2 - a.p;
         const int R = sub_len(a.n, r), C = sub_len(a.n, s), off = class_offset(a.n, 2 * r + s);
         TC acc = 0;
+        constexpr bool HWC = XLayout<TX>::HWC;
+        const int es = HWC ? a.c_in : 1;
         for (int ci = 0; ci < a.c_in; ++ci) {
-            const TX *xc = reinterpret_cast<const TX *>(a.x) + (b * a.c_in + ci) * plane;
+            const TX *xc = reinterpret_cast<const TX *>(a.x) + b * a.c_in * plane + ci * XLayout<TX>::chan(plane);
             const TC *wp = wsrc + ((int64_t)co * a.c_in + ci) * a.n2p + off;
             for (int u = 0; u < R; ++u) {
                 const int ii = bx + u;
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(256) direct_generic_kernel(DirectArgs a) {
                 for (int v = 0; v < C; ++v) {
                     const int jj = by + v;
                     if ((unsigned)jj >= (unsigned)a.w_in) continue;
-                    acc += load_x<TX, TC, RBF>(xc + (int64_t)ii * a.w_in + jj) * wp[u * C + v];
+                    acc += load_x<TX, TC, RBF>(xc + ((int64_t)ii * a.w_in + jj) * es) * wp[u * C + v];
                 }
             }
         }
@@ -317,8 +337,10 @@ __global__ void __launch_bounds__(256) reference_engine_kernel(DirectArgs a, int
         const int co = (idx / ((int64_t)a.ow * a.oh)) % a.c_out;
         const int64_t b = idx / ((int64_t)a.ow * a.oh * a.c_out);
         TC acc = 0;
+        constexpr bool HWC = XLayout<TX>::HWC;
+        const int es = HWC ? a.c_in : 1;
         for (int ci = 0; ci < a.c_in; ++ci) {
-            const TX *xc = reinterpret_cast<const TX *>(a.x) + (b * a.c_in + ci) * plane;
+            const TX *xc = reinterpret_cast<const TX *>(a.x) + b * a.c_in * plane + ci * XLayout<TX>::chan(plane);
             const TC *wp = wsrc + ((int64_t)co * a.c_in + ci) * a.n2p;
             for (int u = 0; u < n; ++u) {
                 const int uu = xo + u - pad;  // index into the un-padded upsampled map
@@ -326,7 +348,8 @@ __global__ void __launch_bounds__(256) reference_engine_kernel(DirectArgs a, int
                 for (int v = 0; v < n; ++v) {
                     const int vv = yo + v - pad;
                     const bool live = rlive && vv >= 0 && (vv & 1) == 0 && (vv >> 1) < a.w_in;
-                    const TC val = live ? load_x<TX, TC, RBF>(xc + (int64_t)(uu >> 1) * a.w_in + (vv >> 1)) : TC(0);
+                    const TC val =
+                        live ? load_x<TX, TC, RBF>(xc + ((int64_t)(uu >> 1) * a.w_in + (vv >> 1)) * es) : TC(0);
                     acc += val * wp[u * n + v];
                 }
             }
@@ -410,5 +433,7 @@ int launch_direct_f32(const DirectArgs &a, bool ref_engine, cudaStream_t st);
 int launch_direct_f64(const DirectArgs &a, bool ref_engine, cudaStream_t st);
 // bf16 compute: x in {f32 (rounded on load), bf16}, y in {f32, bf16}
 int launch_direct_bf16(const DirectArgs &a, int x_dtype, int y_dtype, bool ref_engine, cudaStream_t st);
+// fp32 compute on the interleaved u8 image payload (x: (B, H, W, C), decoded on load)
+int launch_direct_u8(const DirectArgs &a, bool ref_engine, cudaStream_t st);
 
 }  // namespace segb

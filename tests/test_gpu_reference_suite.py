@@ -42,3 +42,30 @@ def test_reference_suites_pass_on_the_gpu_engine(tmp_path):
     assert res.returncode == 0, tail
     calls = json.loads(report.read_text())
     assert calls["forward"] > 1000 and calls["prepare"] > 1000 and calls["counted"] > 10, calls
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "segconv")),
+                    reason="baseline/_ref not installed (tools/install_reference.sh)")
+def test_reference_harness_with_gpu_columns():
+    """the reference's own run_benchmark / emit_report over GAN_SUITE layers, segregated engine on
+    the GPU, GPU columns added"""
+    import json
+
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import segconv
+
+    from integration import segconv_gpu
+    configs = [c for c in segconv.GAN_SUITE if c.name in ("dcgan_l5", "ebgan_l4", "gpgan_l3")]
+    opts = segconv.bench.RunOptions(seed=7, repeats=2, verify=True)
+    report = segconv_gpu.run_benchmark_gpu(segconv, configs, opts, batch=32, compute="fp32")
+    for rec in report.layers:
+        assert rec["error"] is None and rec["equivalence"]["passed"], rec
+        g = rec["gpu"]
+        assert g["batch"] == 32 and g["useful_gmacs"] > 0 and g["kernel"].startswith("K")
+    doc = json.loads(segconv.bench.emit_report(report, "json"))
+    assert doc["format_version"] == 1 and len(doc["layers"]) == 3
+    assert "|" in segconv.bench.emit_report(report, "markdown")
