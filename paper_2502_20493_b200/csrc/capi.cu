@@ -173,7 +173,7 @@ static size_t f16_plane(const segb_layer *L) { return (size_t)L->n * L->n * L->c
 // 3xFP16 weights; the scale exponent is read back once (prepare is synchronous on its stream)
 static int ensure_f16x3_weights(segb_layer *L, bool lazy, cudaStream_t st) {
     const size_t plane = f16_plane(L);
-    const size_t bytes = 2 * 2 * plane + 1024;
+    const size_t bytes = 2 * 2 * plane + kAbsmaxBytes;
     int rc = ensure_layout(L, &L->wf, bytes, lazy, st, "3xFP16 implicit-GEMM", [&](void *p) -> int {
         float *partials = (float *)((char *)p + 4 * plane);
         int r = run_prep_gemm_f16x2(L->bank, L->bank_dtype, L->c_in, L->c_in_pad, L->c_out, L->c_out_pad, L->n, p,

@@ -18,7 +18,8 @@
 
 namespace segb {
 
-constexpr int kAbsmaxBlocks = 148;  // partial maxima written by absmax_partials_kernel
+constexpr int kAbsmaxBlocks = 4 * 148;  // partial maxima written by absmax_partials_kernel (4 blocks per SM)
+constexpr int kAbsmaxBytes = (kAbsmaxBlocks * 4 + 255) / 256 * 256;
 
 // exponent k with max|v| * 2^k < 2^15; 0 for an all-zero or non-finite maximum
 __host__ __device__ inline int f16_scale_exp(float maxabs) {
@@ -53,7 +54,7 @@ template <> __device__ __forceinline__ float absf_of<__nv_bfloat16>(__nv_bfloat1
 
 // per-block max |v| over a grid-strided range; exactly kAbsmaxBlocks blocks
 template <typename T>
-__global__ void __launch_bounds__(512) absmax_partials_kernel(const T *__restrict__ v, int64_t count,
+__global__ void __launch_bounds__(256) absmax_partials_kernel(const T *__restrict__ v, int64_t count,
                                                               float *__restrict__ partials) {
     float m = 0.f;
     if constexpr (sizeof(T) == 4) {
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(512) absmax_partials_kernel(const T *__restric
             m = fmaxf(m, absf_of(v[j]));
     }
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-    __shared__ float wm[16];
+    __shared__ float wm[8];
     if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {

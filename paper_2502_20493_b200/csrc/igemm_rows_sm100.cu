@@ -587,26 +587,25 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             for (int i = lane; i < kAbsmaxBlocks; i += 32) mx = fmaxf(mx, __ldg(prm.x_partials + i));
             for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
             const float sc = ldexpf(1.f, f16_scale_exp(mx));
-            constexpr int KLB = 2;  // units in flight per thread (64 fp32 registers each)
-            auto load_unit = [&](int t, int l, int kb, float4 (&r)[16], float (&hv)[8]) {
+            // all 128 loader threads share a unit: thread (cg = t & 7, c4 = t >> 3) owns 8 channels x
+            // 4 columns (one 16-byte load per channel), so a unit costs each thread 32 values
+            static_assert(MR == 64, "3xFP16 rows: 64-wide tiles (16 column chunks of 4)");
+            const int c4 = tt >> 3;
+            constexpr int KLB = 3;  // units in flight per thread (32 fp32 registers each)
+            auto load_unit = [&](int t, int l, int kb, float4 (&r)[8], float (&hv)[8]) {
                 t += toff;
                 const int i = t % prm.rows, rest = t / prm.rows;
                 const int ms = rest % prm.msub, b = rest / prm.msub;
                 const int row = i + dminr + l;
                 const int j0 = ms * MR;
                 const bool in_row = row >= 0 && row < prm.h;
-                const bool rok = in_row && col_active;
                 const int ch0 = (PAIRKB ? kbt : kb) * 64 + cg * 8;
                 const float *src = xf + ((int64_t)b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    r[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    r[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (rok && ch0 + c < prm.c_in) {
-                        const float4 *p4 = reinterpret_cast<const float4 *>(src + (int64_t)c * plane_in + cc * 8);
-                        r[2 * c] = __ldg(p4);
-                        r[2 * c + 1] = __ldg(p4 + 1);
-                    }
+                    r[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (in_row && ch0 + c < prm.c_in)
+                        r[c] = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)c * plane_in + c4 * 4));
                 }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) hv[c] = 0.f;
@@ -620,7 +619,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     }
                 }
             };
-            float4 rb[KLB][16];
+            float4 rb[KLB][8];
             float hb[KLB][8];
             int bkb[KLB];
             bool bv[KLB];
@@ -647,15 +646,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     const int sidx = qs * KBC + ckb;
                     if (!(ABL(64))) mbar_wait(&slot_empty[sidx], qph ^ 1);
                     const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
-                    if (col_active && !(ABL(16))) {
-                        uint32_t hp[8][4], lp[8][4];  // [channel][k]: columns 2k, 2k+1 as fp16 pairs
+                    if (!(ABL(16))) {
+                        uint32_t hp[8][2], lp[8][2];  // [channel][q]: columns 2q, 2q+1 as fp16 pairs
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
-                            const float v[8] = {rb[k][2 * c].x, rb[k][2 * c].y, rb[k][2 * c].z, rb[k][2 * c].w,
-                                                rb[k][2 * c + 1].x, rb[k][2 * c + 1].y, rb[k][2 * c + 1].z,
-                                                rb[k][2 * c + 1].w};
+                            const float v[4] = {rb[k][c].x, rb[k][c].y, rb[k][c].z, rb[k][c].w};
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
+                            for (int q = 0; q < 2; ++q) {
                                 __half h0, l0, h1, l1;
                                 split_f16(v[2 * q] * sc, h0, l0);
                                 split_f16(v[2 * q + 1] * sc, h1, l1);
@@ -664,7 +661,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                             }
                         }
 #pragma unroll
-                        for (int w = 0; w < 8; ++w) {
+                        for (int w = 0; w < 4; ++w) {  // slot row = column c4*4 + w, 8 channels = 16 B
                             uint32_t oh[4], ol[4];
                             const uint32_t sel = (w & 1) ? 0x7632 : 0x5410;
 #pragma unroll
@@ -672,7 +669,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                                 oh[m4] = __byte_perm(hp[2 * m4][w >> 1], hp[2 * m4 + 1][w >> 1], sel);
                                 ol[m4] = __byte_perm(lp[2 * m4][w >> 1], lp[2 * m4 + 1][w >> 1], sel);
                             }
-                            const int rho = HL + cc * 8 + w;
+                            const int rho = HL + c4 * 4 + w;
                             const uint32_t addr = dst + rho * 128 + ((cg ^ (rho & 7)) << 4);
                             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(oh[0]),
                                          "r"(oh[1]), "r"(oh[2]), "r"(oh[3])
@@ -885,6 +882,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
                 float *pf = reinterpret_cast<float *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE) * plane +
                             (int64_t)(2 * i + row_off) * prm.ow + (int64_t)ms * 2 * MR + 2 * m;
+                const int odd = lane & 1;
+                float *pf4 = pf - 2 * odd + odd * prm.ow;  // even lane: row 2i, col 2m; odd: row 2i+1, col 2m-2
                 constexpr int CH = kEpiChunk;
                 uint32_t v[NCL][CH], v2[NCL][CH];
 #pragma unroll
@@ -905,11 +904,14 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     for (int k = 0; k < CH; ++k) {
                         const float2 r0 = make_float2(__uint_as_float(cur[C00][k]) * us, __uint_as_float(cur[C01][k]) * us);
                         const float2 r1 = make_float2(__uint_as_float(cur[C10][k]) * us, __uint_as_float(cur[C11][k]) * us);
-                        if (lane_active && !(ABL(1))) {
-                            float *q = pf + (int64_t)(co0 + k) * plane;
-                            *reinterpret_cast<float2 *>(q) = r0;
-                            *reinterpret_cast<float2 *>(q + prm.ow) = r1;
-                        }
+                        // 16-byte stores: lanes 2q, 2q+1 (positions j, j+1 = output columns 4q'..4q'+3)
+                        // swap one row's pair, so the even lane writes row 2i and the odd lane row 2i+1
+                        const float2 give = odd ? r0 : r1;
+                        const float2 got = make_float2(__shfl_xor_sync(0xffffffffu, give.x, 1),
+                                                       __shfl_xor_sync(0xffffffffu, give.y, 1));
+                        const float4 v4 = odd ? make_float4(got.x, got.y, r1.x, r1.y) : make_float4(r0.x, r0.y, got.x, got.y);
+                        if (lane_active && !(ABL(1)))
+                            *reinterpret_cast<float4 *>(pf4 + (int64_t)(co0 + k) * plane) = v4;
                     }
                 };
                 for (int co0 = 0; co0 < NE; co0 += 2 * CH) {
@@ -1165,7 +1167,7 @@ static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMa
     cudaLaunchKernelEx(&cfg, kern, tmB, tmBlo, prm);
 }
 
-int64_t igemm_rows_workspace_bytes(const IgemmShape &s) { return rows_f16(s) ? 1024 : 0; }
+int64_t igemm_rows_workspace_bytes(const IgemmShape &s) { return rows_f16(s) ? kAbsmaxBytes : 0; }
 
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,
                    int64_t ws_bytes, cudaStream_t st) {

@@ -714,7 +714,7 @@ int64_t igemm_workspace_bytes(const IgemmShape &s) {
     const int mode = fp32_mode(s);
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
     const int64_t bpe = mode == kModeTf32x3 ? 8 : (mode == kModeF16x3 ? 4 : 2);  // bytes per element, all planes
-    return (elems * bpe + 255) / 256 * 256 + (mode == kModeF16x3 ? 1024 : 0);   // + the absmax partials
+    return (elems * bpe + 255) / 256 * 256 + (mode == kModeF16x3 ? kAbsmaxBytes : 0);  // + the absmax partials
 }
 
 static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const void *ptr, const cuuint64_t *dims,

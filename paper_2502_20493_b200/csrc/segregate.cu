@@ -262,10 +262,10 @@ int run_prep_gemm_tf32(const void *bank, int bank_dtype, int c_in, int c_in_pad,
 namespace segb {
 int run_absmax_partials(const void *v, int dtype, int64_t count, float *partials, cudaStream_t st) {
     switch (dtype) {
-        case SEGB_F32: absmax_partials_kernel<float><<<kAbsmaxBlocks, 512, 0, st>>>((const float *)v, count, partials); break;
-        case SEGB_F64: absmax_partials_kernel<double><<<kAbsmaxBlocks, 512, 0, st>>>((const double *)v, count, partials); break;
+        case SEGB_F32: absmax_partials_kernel<float><<<kAbsmaxBlocks, 256, 0, st>>>((const float *)v, count, partials); break;
+        case SEGB_F64: absmax_partials_kernel<double><<<kAbsmaxBlocks, 256, 0, st>>>((const double *)v, count, partials); break;
         case SEGB_BF16:
-            absmax_partials_kernel<__nv_bfloat16><<<kAbsmaxBlocks, 512, 0, st>>>((const __nv_bfloat16 *)v, count, partials);
+            absmax_partials_kernel<__nv_bfloat16><<<kAbsmaxBlocks, 256, 0, st>>>((const __nv_bfloat16 *)v, count, partials);
             break;
         default: return fail(SEGB_ERR_VALUE, "unknown dtype %d", dtype);
     }
