@@ -81,6 +81,8 @@ struct RowsParams {
     uint32_t slot_plane, b_plane;  // byte offset of the lo plane in a slot / in the weight area
     const float *x_partials;
     float w_unscale;               // 2^-k_w of the weight planes
+    int ch_base;                   // F16: first input channel of this pass (c_in > 64 runs 64-channel passes)
+    int accumulate;                // F16: add this pass's sums to y (passes after the first)
 };
 
 // Role ablation for bottleneck experiments, compiled in only with -DSEGB_ROWS_ABLATION
@@ -318,7 +320,7 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
                 for (int kb = 0; kb < KBC; ++kb)
                     for (int pl = 0; pl < planes; ++pl)
                         tma_load_3d_2sm(sB + pl * prm.b_plane + (kb * SCH.ntiles + g.b0 + j) * prm.b_tile_bytes,
-                                        pl ? tmBlo : tmB, lb, kb * 64, co_off, tap);
+                                        pl ? tmBlo : tmB, lb, prm.ch_base + kb * 64, co_off, tap);
             }
         }
         return;
@@ -333,7 +335,7 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
             for (int kb = 0; kb < KBC; ++kb)
                 for (int pl = 0; pl < planes; ++pl)
                     tma_load_3d_2sm(sB + pl * prm.b_plane + (kb * SCH.ntiles + k) * prm.b_tile_bytes, pl ? tmBlo : tmB,
-                                    lb, kb * 64, pair_rank * (prm.c_out / 2), tap);
+                                    lb, prm.ch_base + kb * 64, pair_rank * (prm.c_out / 2), tap);
         }
         return;
     }
@@ -345,7 +347,7 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
         for (int kb = 0; kb < KBC; ++kb)
             for (int pl = 0; pl < planes; ++pl)
                 tma_load_3d(sB + pl * prm.b_plane + (kb * SCH.ntiles + k) * prm.b_tile_bytes, pl ? tmBlo : tmB, bar,
-                            kb * 64, 0, tap);
+                            prm.ch_base + kb * 64, 0, tap);
     }
 }
 
@@ -599,7 +601,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 const int row = i + dminr + l;
                 const int j0 = ms * MR;
                 const bool in_row = row >= 0 && row < prm.h;
-                const int ch0 = (PAIRKB ? kbt : kb) * 64 + cg * 8;
+                const int ch0 = prm.ch_base + (PAIRKB ? kbt : kb) * 64 + cg * 8;
                 const float *src = xf + ((int64_t)b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -889,6 +891,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
                 for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE, v[c]);
                 auto chunk = [&](int co0, uint32_t (&cur)[NCL][CH], uint32_t (&nxt)[NCL][CH]) {
+                    // a later channel pass adds to y: the chunk's old values are loaded first, all
+                    // CH in flight at once (interleaved with the stores they would be serialised:
+                    // the compiler cannot prove the plane-strided addresses distinct)
+                    float4 old[CH];
+                    if (prm.accumulate && lane_active) {
+#pragma unroll
+                        for (int k = 0; k < CH; ++k)
+                            old[k] = __ldcs(reinterpret_cast<const float4 *>(pf4 + (int64_t)(co0 + k) * plane));
+                    }
                     tmem_wait_ld();
 #pragma unroll
                     for (int c = 0; c < NCL; ++c) reg_fence_chunk(cur[c]);
@@ -910,8 +921,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         const float2 got = make_float2(__shfl_xor_sync(0xffffffffu, give.x, 1),
                                                        __shfl_xor_sync(0xffffffffu, give.y, 1));
                         const float4 v4 = odd ? make_float4(got.x, got.y, r1.x, r1.y) : make_float4(r0.x, r0.y, got.x, got.y);
-                        if (lane_active && !(ABL(1)))
-                            *reinterpret_cast<float4 *>(pf4 + (int64_t)(co0 + k) * plane) = v4;
+                        if (lane_active && !(ABL(1))) {
+                            float4 *dst4 = reinterpret_cast<float4 *>(pf4 + (int64_t)(co0 + k) * plane);
+                            if (prm.accumulate) {  // a later channel pass: y += this pass's sums
+                                const float4 o = old[k];
+                                *dst4 = make_float4(o.x + v4.x, o.y + v4.y, o.z + v4.z, o.w + v4.w);
+                            } else {
+                                *dst4 = v4;
+                            }
+                        }
                     }
                 };
                 for (int co0 = 0; co0 < NE; co0 += 2 * CH) {
@@ -1029,7 +1047,9 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     const bool f16 = rows_f16(s);
     if (f16) {  // 3xFP16: fp32 in / out, one channel block, the 2-SM pair over batch halves
         if (s.x_dtype != SEGB_F32 || s.y_dtype != SEGB_F32) return false;
-        if (s.n != 4 || s.c_in > 64 || s.c_in % 8 != 0 || s.batch % 2 != 0 || s.c_out % 32 != 0) return false;
+        // c_in > 64: 64-channel passes, the later ones accumulating into y (the weights of one
+        // channel block, hi and lo, fill half the shared memory of each CTA of the pair)
+        if (s.n != 4 || s.c_in > 128 || s.c_in % 8 != 0 || s.batch % 2 != 0 || s.c_out % 32 != 0) return false;
     } else if (s.compute != SEGB_BF16) {
         return false;
     }
@@ -1070,7 +1090,7 @@ static bool rows_params(const IgemmShape &s, RowsParams &prm, int &nh, int &kbc,
     prm.dmin_c = dmin_c;
     prm.slot_rows = mr + dmax_c - dmin_c;
     if (-dmin_c > 8 || dmax_c > 8) return false;
-    kbc = (s.c_in + 63) / 64;
+    kbc = f16 ? 1 : (s.c_in + 63) / 64;  // F16: per pass
     if (kbc > 2) return false;
     prm.slot_bytes = (prm.slot_rows * 128 + 1023) / 1024 * 1024;
     prm.slot_plane = prm.b_plane = 0;
@@ -1209,6 +1229,8 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, const voi
     prm.y = y;
     prm.prof = nullptr;
     prm.ablate = 0;
+    prm.ch_base = 0;
+    prm.accumulate = 0;
     if (const char *ab = getenv("SEGB200_ABLATE")) prm.ablate = atoi(ab);
     if (const char *rg = getenv("SEGB200_ROWS_RING")) {  // debug: cap the ring depth
         const int nr_cta = nsplit == 2 ? nh : prm.nr;
@@ -1244,9 +1266,16 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, const voi
         launch_rows<NH_, KBC_, SW_, MR_, NS_>(grid, smem, st, tmB, tmBlo, prm);                    \
     else
     // 3xFP16 (fp32 in / out): EB-GAN l7's shape family
-    if (f16 && nh == 2 && kbc == 1 && swap == 0 && mr == 64 && nsplit == 3)
-        launch_rows<2, 1, 0, 64, 3, true>(grid, smem, st, tmB, tmBlo, prm);
-    else
+    if (f16 && nh == 2 && kbc == 1 && swap == 0 && mr == 64 && nsplit == 3) {
+        // one launch per 64-channel block of the input, the later ones accumulating into y
+        const int passes = (s.c_in + 63) / 64;
+        for (int ps = 0; ps < passes; ++ps) {
+            prm.ch_base = 64 * ps;
+            prm.accumulate = ps > 0;
+            launch_rows<2, 1, 0, 64, 3, true>(grid, smem, st, tmB, tmBlo, prm);
+            if (ps + 1 < passes) note_launch();
+        }
+    } else
     // instantiated: n in {2, 4, 6} x channel blocks x P parity for 128-wide rows; the n = 4
     // (GAN) family also for 64-wide rows and with the row-parity split
     SEGB_ROWS_CASE(1, 1, 0, 128, 1) SEGB_ROWS_CASE(1, 1, 1, 128, 1) SEGB_ROWS_CASE(1, 2, 0, 128, 1)

@@ -697,7 +697,10 @@ bool igemm_supported(const IgemmShape &s) {
 
 const char *igemm_kernel_name(const IgemmShape &s) {
     if (igemm_scatter_supported(s)) return "K3c scatter-GEMM + gather (bf16)";
-    if (use_rows(s)) return s.compute == SEGB_F32 ? "K3b row-streaming GEMM (3xFP16)" : "K3b row-streaming GEMM (bf16)";
+    if (use_rows(s))
+        return s.compute != SEGB_F32 ? "K3b row-streaming GEMM (bf16)"
+               : s.c_in > 64         ? "K3b row-streaming GEMM (3xFP16, 64-channel passes)"
+                                     : "K3b row-streaming GEMM (3xFP16)";
     const int mode = fp32_mode(s);
     if (mode == kModeF16x3) return "K3 implicit GEMM (3xFP16)";
     if (mode == kModeTf32x3) return "K3 implicit GEMM (3xTF32)";

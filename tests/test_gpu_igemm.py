@@ -358,6 +358,8 @@ ROWS_F16_CASES = [  # K3b row-streaming 3xFP16 (fp32 in / out): 2-SM pairs over 
     ("c_out32", 16, 64, 64, 4, 32, 2, 2),
     ("h4_b2", 4, 64, 64, 4, 64, 2, 2),
     ("b6_h8", 8, 128, 64, 4, 64, 2, 6),
+    ("ebgan_l6_b2", 64, 64, 128, 4, 64, 2, 2),   # two 64-channel passes, the second accumulating
+    ("c_in96_c32", 16, 64, 96, 4, 32, 2, 4),     # a partial second channel block
 ]
 
 
