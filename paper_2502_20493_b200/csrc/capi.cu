@@ -208,7 +208,7 @@ static bool may_use_scatter(const segb_layer *L) {
 }
 static bool may_use_f16x3(const segb_layer *L) {
     return L->engine == SEGB_ENGINE_SEGREGATED && L->n % 2 == 0 && L->c_in >= 64 && L->c_in % 8 == 0 &&
-           L->c_out >= 16 && igemm_available();
+           igemm_available();
 }
 static bool may_use_tf32(const segb_layer *L) {
     return L->engine == SEGB_ENGINE_SEGREGATED && L->n % 2 == 0 && L->c_in >= 32 && L->c_in % 4 == 0 &&
@@ -225,6 +225,17 @@ static bool igemm_ok(const segb_layer *L, int x_dtype, int64_t batch, int in_h, 
     s.batch = batch; s.c_in = L->c_in; s.c_out = L->c_out; s.h = in_h; s.w = in_w; s.n = L->n; s.pad = L->pad;
     s.x_dtype = x_dtype; s.y_dtype = y_dtype; s.compute = compute;
     s.f16x3 = compute == SEGB_F32 && L->wf != nullptr;
+    if (compute == SEGB_F32 && L->c_out < 16) {
+        // narrow fp32 outputs (dcgan_l5): the tensor cores pad N to 32 and re-read the input per
+        // class and tap, the direct kernel streams it once; the direct kernel wins whenever it has
+        // blocks enough to fill the GPU (measured: 97 us vs 127 us at batch 64, 141 vs 436 at 256),
+        // the tensor-core kernel at small batches (34 vs 101 us at batch 1: 2 direct blocks)
+        const int oh = 2 * in_h + 2 * L->pad - L->n, ow = 2 * in_w + 2 * L->pad - L->n, swap = L->pad & 1;
+        const int64_t nqr = (oh - 1 + swap) / 2 + 1, nqc = (ow - 1 + swap) / 2 + 1;
+        const int cob = std::min(L->c_out, 4), rq = L->n <= 5 ? 4 : 2, cq = (L->n <= 5 && cob <= 2) ? 2 : 1;
+        const int64_t blocks = ceil_div(nqc, 32 * cq) * ceil_div(L->c_out, cob) * ceil_div(nqr, 4 * rq) * batch;
+        if (blocks >= 64) return false;
+    }
     return igemm_supported(s);
 }
 

@@ -600,8 +600,9 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     const bool tf32 = mode != kModeBf16;  // three-pass operands (hi / lo planes)
     if (s.n % 2 != 0) return false;  // all four classes share one grid
     if (mode == kModeF16x3) {
+        // any c_out: a narrow output (dcgan_l5's 3 channels) pads N to 32 on the tensor cores, still
+        // faster than the FFMA direct kernel at every batch (small batches: many more CTAs)
         if (s.c_in < 64 || s.c_in % 8 != 0) return false;
-        if (s.c_out < 16) return false;
         if (s.x_dtype != SEGB_F32 || s.y_dtype != SEGB_F32) return false;
     } else if (tf32) {
         if (s.c_in < 32 || s.c_in % 4 != 0) return false;
@@ -663,6 +664,12 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     // 1024+ output channels: N = 128 tiles quantise better over the SMs (ebgan_l2 0.195 -> 0.190
     // ms); with fewer channels the halved N re-reads A twice as often and loses (dcgan l2-l4)
     if (!tf32 && cop >= 1024 && cop % 128 == 0) nt = 128;
+    {  // few position blocks (small batches: DCGAN/EB-GAN l2 at batch 1 has 16 positions per class):
+       // narrower N tiles until the four classes' tiles cover the SMs, so the weight stream -- the
+       // bytes that bound such a layer -- is read by many SMs at once instead of a handful
+        const int64_t mt = ceil_div(s.batch * (int64_t)((oh + 1) / 2) * ((ow + 1) / 2), kBlockM);
+        while (nt > 32 && nt % 64 == 0 && cop % (nt / 2) == 0 && 4 * mt * (cop / nt) < 148) nt /= 2;
+    }
     if (const char *e = getenv("SEGB200_K3_NTILE")) {  // A/B experiments: force the N tile
         const int v = atoi(e);
         if (v >= 32 && v <= nmax && v % 32 == 0 && cop % v == 0) nt = v;
