@@ -593,20 +593,47 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             // 4 columns (one 16-byte load per channel), so a unit costs each thread 32 values
             static_assert(MR == 64, "3xFP16 rows: 64-wide tiles (16 column chunks of 4)");
             const int c4 = tt >> 3;
-            constexpr int KLB = 3;  // units in flight per thread (32 fp32 registers each)
-            auto load_unit = [&](int t, int l, int kb, float4 (&r)[8], float (&hv)[8]) {
-                t += toff;
-                const int i = t % prm.rows, rest = t / prm.rows;
-                const int ms = rest % prm.msub, b = rest / prm.msub;
-                const int row = i + dminr + l;
-                const int j0 = ms * MR;
+#ifndef SEGB_ROWS_F16_KLB
+#define SEGB_ROWS_F16_KLB 3
+#endif
+            constexpr int KLB = SEGB_ROWS_F16_KLB;  // units in flight per thread (32 fp32 registers each)
+            // unit cursor with its tile's (row i, segment ms, sample b) kept incrementally: no
+            // runtime divisions per unit
+            struct Cur {
+                int t, l, i, ms, b;
+            };
+            auto cur_at = [&](int t) {
+                Cur c;
+                c.t = t;
+                c.l = t < t1 ? nr - loads_of(t) : 0;
+                const int ta = t + toff;
+                c.i = ta % prm.rows;
+                const int rest = ta / prm.rows;
+                c.ms = rest % prm.msub;
+                c.b = rest / prm.msub;
+                return c;
+            };
+            auto cur_next = [&](Cur &c) {
+                if (++c.l < nr) return;
+                if (++c.t >= t1) return;
+                if (++c.i == prm.rows) {  // a new strip: its first tile loads all nr rows
+                    c.i = 0;
+                    if (++c.ms == prm.msub) { c.ms = 0; ++c.b; }
+                    c.l = 0;
+                } else {
+                    c.l = nr - 1;  // consecutive tiles of a strip share nr - 1 rows
+                }
+            };
+            auto load_unit = [&](const Cur &u, float4 (&r)[8], float (&hv)[8]) {
+                const int row = u.i + dminr + u.l;
+                const int j0 = u.ms * MR;
                 const bool in_row = row >= 0 && row < prm.h;
-                const int ch0 = prm.ch_base + (PAIRKB ? kbt : kb) * 64 + cg * 8;
-                const float *src = xf + ((int64_t)b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
+                const int ch0 = prm.ch_base + cg * 8;
+                const float *src = xf + ((int64_t)u.b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     r[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (in_row && ch0 + c < prm.c_in)
+                    if (in_row && ch0 + c < prm.c_in && !(ABL(2)))
                         r[c] = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)c * plane_in + c4 * 4));
                 }
 #pragma unroll
@@ -621,18 +648,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     }
                 }
             };
+            static_assert(KBC == 1 && !PAIRKB, "3xFP16 rows: one 64-channel block per pass");
             float4 rb[KLB][8];
             float hb[KLB][8];
-            int bkb[KLB];
             bool bv[KLB];
-            int ct = t0, cl = t0 < t1 ? nr - loads_of(t0) : 0, ckb_ = 0;
+            Cur cu = cur_at(t0);
 #pragma unroll
             for (int k = 0; k < KLB; ++k) {
-                bv[k] = ct < t1;
-                bkb[k] = ckb_;
+                bv[k] = cu.t < t1;
                 if (bv[k]) {
-                    load_unit(ct, cl, ckb_, rb[k], hb[k]);
-                    advance(ct, cl, ckb_);
+                    load_unit(cu, rb[k], hb[k]);
+                    cur_next(cu);
                 }
             }
             uint32_t qs = 0, qph = 0;
@@ -644,23 +670,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         more = false;
                         break;
                     }
-                    const int ckb = PAIRKB ? kbt : bkb[k];
-                    const int sidx = qs * KBC + ckb;
+                    const int sidx = qs;
                     if (!(ABL(64))) mbar_wait(&slot_empty[sidx], qph ^ 1);
                     const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
                     if (!(ABL(16))) {
                         uint32_t hp[8][2], lp[8][2];  // [channel][q]: columns 2q, 2q+1 as fp16 pairs
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
-                            const float v[4] = {rb[k][c].x, rb[k][c].y, rb[k][c].z, rb[k][c].w};
+                            const float v[4] = {rb[k][c].x * sc, rb[k][c].y * sc, rb[k][c].z * sc, rb[k][c].w * sc};
 #pragma unroll
-                            for (int q = 0; q < 2; ++q) {
-                                __half h0, l0, h1, l1;
-                                split_f16(v[2 * q] * sc, h0, l0);
-                                split_f16(v[2 * q + 1] * sc, h1, l1);
-                                hp[c][q] = pack_h2(h0, h1);
-                                lp[c][q] = pack_h2(l0, l1);
-                            }
+                            for (int q = 0; q < 2; ++q)  // packed conversions, bitwise split_f16's
+                                split_f16x2(v[2 * q], v[2 * q + 1], hp[c][q], lp[c][q]);
                         }
 #pragma unroll
                         for (int w = 0; w < 4; ++w) {  // slot row = column c4*4 + w, 8 channels = 16 B
@@ -707,14 +727,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));
                         else mbar_arrive(&slot_full[sidx]);
                     }
-                    if (PAIRKB || ckb == KBC - 1) {
-                        if (++qs == (uint32_t)ring) { qs = 0; qph ^= 1; }
-                    }
-                    bv[k] = ct < t1;
-                    bkb[k] = ckb_;
+                    if (++qs == (uint32_t)ring) { qs = 0; qph ^= 1; }
+                    bv[k] = cu.t < t1;
                     if (bv[k]) {
-                        load_unit(ct, cl, ckb_, rb[k], hb[k]);
-                        advance(ct, cl, ckb_);
+                        load_unit(cu, rb[k], hb[k]);
+                        cur_next(cu);
                     }
                 }
             }
@@ -888,6 +905,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 float *pf4 = pf - 2 * odd + odd * prm.ow;  // even lane: row 2i, col 2m; odd: row 2i+1, col 2m-2
                 constexpr int CH = kEpiChunk;
                 uint32_t v[NCL][CH], v2[NCL][CH];
+                if (ABL(8)) {  // ablation: no TMEM reads (nor stores)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0 && !(ABL(32))) release_acc(acc);
+                    if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+                    continue;
+                }
 #pragma unroll
                 for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE, v[c]);
                 auto chunk = [&](int co0, uint32_t (&cur)[NCL][CH], uint32_t (&nxt)[NCL][CH]) {
