@@ -86,6 +86,42 @@ __global__ void __launch_bounds__(128, 1) mma_peak(int kind, int iters, long lon
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// FFMA with all three operands in registers (the direct kernel's x * w + acc), and its packed
+// FFMA2 form (two fp32 FMAs per lane per instruction, sm_100)
+__global__ void __launch_bounds__(256) ffma_reg_peak(int iters, const float *bw, float *out) {
+    float a[16];
+    const float b = bw[threadIdx.x & 7], c = bw[8 + (threadIdx.x & 7)];
+    float bb[16], cr[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { a[k] = threadIdx.x * 1e-7f + k; bb[k] = b + k * 1e-9f; cr[k] = c - k * 1e-9f; }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) a[k] = fmaf(bb[k], a[k], cr[k]);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += a[k];
+    if (s == 12345.f) out[threadIdx.x] = s;
+}
+__global__ void __launch_bounds__(256) ffma2_peak(int iters, const float *bw, float *out) {
+    float2 a[8], bb[8];
+    const float b = bw[threadIdx.x & 7], c = bw[8 + (threadIdx.x & 7)];
+    const float2 cc = make_float2(c, c);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        a[k] = make_float2(threadIdx.x * 1e-7f + k, k + 0.5f);
+        bb[k] = make_float2(b + k * 1e-9f, b - k * 1e-9f);
+    }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __ffma2_rn(bb[k], a[k], cc);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k].x + a[k].y;
+    if (s == 12345.f) out[threadIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) ffma_peak(int iters, float *out) {
     float a[16];
 #pragma unroll
@@ -163,6 +199,30 @@ int main() {
             if (tf > best) best = tf;
         }
         printf(", \"ffma\": {\"tflops\": %.1f}", best);
+    }
+    {  // register-operand FFMA and FFMA2
+        float hb[16];
+        for (int i = 0; i < 16; ++i) hb[i] = 0.999f + i * 1e-6f;
+        float *dbw;
+        cudaMalloc(&dbw, sizeof hb);
+        cudaMemcpy(dbw, hb, sizeof hb, cudaMemcpyHostToDevice);
+        const int iters = 1 << 14, blocks = sms * 8;
+        for (int v = 0; v < 2; ++v) {
+            double best = 0;
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(e0);
+                if (v == 0) ffma_reg_peak<<<blocks, 256>>>(iters, dbw, df);
+                else ffma2_peak<<<blocks, 256>>>(iters, dbw, df);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e0, e1);
+                const double flop = 2.0 * 16 * iters * 256.0 * blocks;
+                const double tf = flop / (ms * 1e-3) / 1e12;
+                if (tf > best) best = tf;
+            }
+            printf(", \"%s\": {\"tflops\": %.1f}", v == 0 ? "ffma_reg" : "ffma2_reg", best);
+        }
     }
     printf("}\n");
     return 0;

@@ -4,7 +4,10 @@ reports), after an untimed warm-up of all of them:
     python tools/profile_set.py ebgan_l7:fp32:256 ds512_k5:fp32:64 dcgan_l2:bf16:256 ...
 
 Each spec is name:dtype:batch (name from bench.py's layer tables). The script prints the kernel
-family each layer dispatches to, in launch order, so ncu's launch list can be matched to layers.
+family each layer dispatches to, in launch order; before each measured layer it launches a
+one-element unit_floats kernel as a marker, so a capture filtered with
+-k 'regex:unit_floats|direct_kernel|igemm|scatter|absmax|nchw_to_nhwc' splits into layers
+(tools/ncu_summary.py).
 """
 import os
 import sys
@@ -35,6 +38,9 @@ def main():
         layer.forward(x, out=y)
     torch.cuda.synchronize()
     for spec, layer, x, y in runs:
+        # a one-element unit_floats launch marks where each layer's launches start (include
+        # "unit_floats" in ncu's -k filter; tools/ncu_summary.py splits on it)
+        device_unit_floats((1,), 0)
         print(f"{spec}: {layer.describe_path(x.shape[0], x.shape[2], x.shape[3])}", flush=True)
         layer.forward(x, out=y)
         torch.cuda.synchronize()
