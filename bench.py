@@ -89,8 +89,10 @@ def load_peaks():
         out.update(hbm_gbs=d["hbm_gbs"], bf16_tflops=d["bf16_tflops"], source="measured (MEASURED_PEAKS.json)")
     with open(os.path.join(ROOT, "profiles", "r2_peaks.json")) as f:
         p = json.load(f)
+    # the FP32 FMA roof of the direct kernel: register-operand FFMA2 (packed, two FMAs per lane), the
+    # fastest FMA form with operands in registers (the immediate-operand FFMA peak does not apply)
     out.update(tf32_mma_tflops=p["tf32_mma_tflops"], fp16_mma_tflops=p["fp16_mma_tflops"],
-               ffma_tflops=p["ffma_tflops"])
+               ffma_tflops=p.get("ffma2_reg_tflops", p["ffma_tflops"]))
     return out
 
 
@@ -114,7 +116,7 @@ def compute_roof(kernel: str, peaks: dict):
         if "3xTF32" in kernel:  # three kind::tf32 MMAs per product
             return peaks["tf32_mma_tflops"] / 3.0, "tensor (3xTF32: tf32 MMA ceiling / 3, measured)"
         return peaks["bf16_tflops"], "tensor (bf16, MEASURED_PEAKS)"
-    return peaks["ffma_tflops"], "fp32 FFMA (measured)"
+    return peaks["ffma_tflops"], "fp32 FMA (register-operand FFMA2, measured)"
 
 
 # ---------------------------------------------------------------------------------------
