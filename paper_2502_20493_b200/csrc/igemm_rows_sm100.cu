@@ -892,10 +892,27 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             const int64_t plane = (int64_t)prm.oh * prm.ow;
             constexpr int C00 = class_slot(2 * RE + SE), C01 = class_slot(2 * RE + (1 - SE));
             constexpr int C10 = class_slot(2 * (1 - RE) + SE), C11 = class_slot(2 * (1 - RE) + (1 - SE));
+            // a later channel pass reads y back: the next tile's lines of this warp (32 channels x 2
+            // rows x 256 B) are prefetched into L2 while this tile's accumulators are awaited
+            auto prefetch_tile = [&](int tn) {
+                const int ta = tn + toff;
+                const int i = ta % prm.rows, rest = ta / prm.rows;
+                const int ms = rest % prm.msub, b = rest / prm.msub;
+                const float *base = reinterpret_cast<const float *>(prm.y) +
+                                    ((int64_t)b * prm.c_out + chalf * NE + lane % NE) * plane +
+                                    (int64_t)(2 * i + row_off) * prm.ow + (int64_t)ms * 2 * MR + 2 * ((quarter & 1) * 32);
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)r * prm.ow + h * 32));
+            };
+            if (prm.accumulate && t0 < t1) prefetch_tile(t0);
             for (int t = t0; t < t1; ++t) {
                 const int ta = t + toff;
                 const int i = ta % prm.rows, rest = ta / prm.rows;
                 const int ms = rest % prm.msub, b = rest / prm.msub;
+                if (prm.accumulate && t + 1 < t1) prefetch_tile(t + 1);
                 if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
