@@ -653,6 +653,23 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             float hb[KLB][8];
             bool bv[KLB];
             Cur cu = cur_at(t0);
+            // L2 prefetch of the row unit kPrefetch units beyond the register loads: each of the 128
+            // threads touches one of the unit's 128-byte lines (64 channels x 2 halves of the row)
+#ifndef SEGB_ROWS_F16_PREFETCH
+#define SEGB_ROWS_F16_PREFETCH 4
+#endif
+            constexpr int kPrefetch = SEGB_ROWS_F16_PREFETCH;
+            Cur pc = cu;
+            auto prefetch_unit = [&](const Cur &u) {
+                const int row = u.i + dminr + u.l;
+                if (u.t >= t1 || row < 0 || row >= prm.h) return;
+                const int ch = prm.ch_base + (tt >> 1);
+                if (ch >= prm.c_in) return;
+                const float *p = xf + ((int64_t)u.b * prm.c_in + ch) * plane_in + (int64_t)row * prm.w + u.ms * MR +
+                                 (tt & 1) * 32;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            };
+            for (int k = 0; k < KLB + kPrefetch && pc.t < t1; ++k) cur_next(pc);
 #pragma unroll
             for (int k = 0; k < KLB; ++k) {
                 bv[k] = cu.t < t1;
@@ -732,6 +749,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     if (bv[k]) {
                         load_unit(cu, rb[k], hb[k]);
                         cur_next(cu);
+                        if (kPrefetch > 0) {
+                            prefetch_unit(pc);
+                            cur_next(pc);
+                        }
                     }
                 }
             }
