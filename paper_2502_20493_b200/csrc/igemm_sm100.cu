@@ -77,6 +77,9 @@ struct IgemmParams {
     void *y;
     const float *x_partials;  // 3xFP16: the input's partial maxima (its scale 2^k_x)
     float w_unscale;          // 3xFP16: 2^-k_w of the weight planes
+    int swap_ab;              // PM 3: weights as the M = 128 side, the few class positions as N
+    int ksplit;               // > 1: each tile covers 1/ksplit of K and writes fp32 partial sums
+    float *partial;           // ksplit: [ks][class][c_out][class position] fp32 partials
 };
 
 template <typename TY> __device__ __forceinline__ TY cvt_out(float v);
@@ -109,7 +112,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int KCH = kstep_channels<MODE>();
     constexpr int NOP = TF32X3 ? 2 : 1;  // tiles per operand per stage (hi [, lo])
     constexpr int CHUNK = MODE == kModeF16x3 ? kF16Chunk : kTf32Chunk;  // k-steps per TMEM partial
-    constexpr bool PAIR = PM > 0, TWO = PM == 2;
+    // PM 3 (SWAP): a single CTA with the operands swapped -- A = 128 output channels of weights,
+    // B = the tile's class positions (N = 16..128): tiny batches, where a 128-position A box would be
+    // mostly zero fill and the weights are the bytes that matter
+    constexpr bool PAIR = PM == 1 || PM == 2, TWO = PM == 2, SWAP = PM == 3;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for SWIZZLE_128B atoms
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -132,9 +138,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // tile iteration: the pair index walks the pair tiles, both CTAs of a pair in lockstep
     const int t_begin = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
     const int t_step = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    // K range of a tile: with split K, tile t covers k-steps [k_lo, k_hi) of its class
+    auto krange = [&](int t, int &k_lo, int &k_hi) {
+        const ClassGeom &g = prm.cls[t & 3];
+        const int nks = g.R * g.C * prm.k_cblocks;
+        if (prm.ksplit <= 1) { k_lo = 0; k_hi = nks; return; }
+        const int ks = (t >> 2) % prm.ksplit, chunk = (nks + prm.ksplit - 1) / prm.ksplit;
+        k_lo = min(nks, ks * chunk);
+        k_hi = min(nks, k_lo + chunk);
+    };
     auto decode = [&](int t, int &c, int &mb, int &nb) {
         c = t & 3;
-        const int rest = t >> 2;
+        const int rest = (t >> 2) / prm.ksplit;
         if (PAIR) {
             mb = 2 * (rest % prm.m_pairs) + rank;
             nb = rest / prm.m_pairs;
@@ -201,14 +216,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int c, mb, nb;
                 decode(t, c, mb, nb);
                 const ClassGeom &g = prm.cls[c];
-                const int64_t P0 = (int64_t)mb * kBlockM;  // past the last block: zero-filled boxes
+                const int64_t P0 = (int64_t)mb * (SWAP ? N : kBlockM);  // past the last block: zero-filled boxes
                 const int64_t per = (int64_t)g.rows * g.cols;
                 const int b0 = (int)(P0 / per);
                 const int rem = (int)(P0 - b0 * per);
                 const int i0 = rem / g.cols, j0 = rem % g.cols;
-                for (int u = 0; u < g.R; ++u)
-                    for (int v = 0; v < g.C; ++v)
-                        for (int kb = 0; kb < prm.k_cblocks; ++kb) {
+                int k_lo, k_hi;
+                krange(t, k_lo, k_hi);
+                for (int kf = k_lo; kf < k_hi; ++kf) {
+                            const int kb = kf % prm.k_cblocks, uv = kf / prm.k_cblocks;
+                            const int u = uv / g.C, v = uv % g.C;
                             mbar_wait(&empty[stage], phase ^ 1);
                             const int wa = j0 + g.base_s + v - prm.p, ha = i0 + g.base_r + u - prm.p;
                             const int tap = g.tap0 + u * g.C + v;
@@ -227,6 +244,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 continue;
                             }
                             mbar_expect_tx(&full[stage], NOP * (a_bytes + b_bytes));
+                            if (SWAP) {  // A: 128 channels of the tap's weights; B: the positions
+                                tma_load_3d(sA + stage * NOP * a_bytes, &tmB, &full[stage], kb * KCH, nb * kBlockM, tap);
+                                tma_load_4d(sB + stage * NOP * b_bytes, &tmA, &full[stage], kb * KCH, wa, ha, b0);
+                                if (TF32X3) {
+                                    tma_load_3d(sA + (stage * NOP + 1) * a_bytes, &tmBlo, &full[stage], kb * KCH,
+                                                nb * kBlockM, tap);
+                                    tma_load_4d(sB + (stage * NOP + 1) * b_bytes, &tmAlo, &full[stage], kb * KCH, wa, ha,
+                                                b0);
+                                }
+                                if (++stage == S_) { stage = 0; phase ^= 1; }
+                                continue;
+                            }
                             tma_load_4d(sA + stage * NOP * a_bytes, &tmA, &full[stage], kb * KCH, wa, ha, b0);
                             if (TF32X3)
                                 tma_load_4d(sA + (stage * NOP + 1) * a_bytes, &tmAlo, &full[stage], kb * KCH, wa, ha, b0);
@@ -265,8 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
             };
             for (int t = t_begin; t < prm.total_tiles; t += t_step) {
-                const ClassGeom &g = prm.cls[t & 3];
-                const int ksteps = g.R * g.C * prm.k_cblocks;
+                int k_lo, k_hi;
+                krange(t, k_lo, k_hi);
+                const int ksteps = k_hi - k_lo;
                 uint32_t d = 0;
                 for (int ks = 0; ks < ksteps; ++ks) {
                     // 3xTF32 accumulates at most kTf32Chunk k-steps per TMEM partial (the
@@ -308,12 +338,68 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t acc_phase = 0;
             const uint32_t lt[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
             for (int t = t_begin; t < prm.total_tiles; t += t_step) {
-                const ClassGeom &g = prm.cls[t & 3];
-                const int uses = TF32X3 ? (g.R * g.C * prm.k_cblocks + CHUNK - 1) / CHUNK : 1;
+                int k_lo, k_hi;
+                krange(t, k_lo, k_hi);
+                const int uses = TF32X3 ? (k_hi - k_lo + CHUNK - 1) / CHUNK : 1;
                 for (int k = 0; k < uses; ++k) {
                     mbar_wait(&tempty[acc], acc_phase);
                     mbar_arrive_cluster(lt[acc]);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
+            }
+        }
+    } else if (SWAP) {  // ---------------- epilogue, swapped: TMEM lane = output channel, column = position
+        const int q = warp & 3;
+        const float unscale = MODE == kModeF16x3 ? *unscale_slot : 1.f;
+        const int64_t plane = (int64_t)prm.oh * prm.ow;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = t_begin; t < prm.total_tiles; t += t_step) {
+            int c, mb, nb;
+            decode(t, c, mb, nb);
+            const ClassGeom &g = prm.cls[c];
+            int k_lo, k_hi;
+            krange(t, k_lo, k_hi);
+            const int nchunks = TF32X3 ? (k_hi - k_lo + CHUNK - 1) / CHUNK : 1;
+            const int co = nb * kBlockM + q * 32 + lane;
+            float racc[kTf32MaxN];
+#pragma unroll
+            for (int k = 0; k < kTf32MaxN; ++k) racc[k] = 0.f;
+            for (int pc = 0; pc < nchunks; ++pc) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+#pragma unroll
+                for (int ch = 0; ch < kTf32MaxN / 16; ++ch) {
+                    if (ch * 16 < N) {
+                        uint32_t v[16];
+                        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * N + ch * 16, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) racc[ch * 16 + k] += __uint_as_float(v[k]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) release_acc(acc);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+            if (co < prm.c_out) {
+                const int64_t per = (int64_t)g.rows * g.cols;
+#pragma unroll
+                for (int k = 0; k < kTf32MaxN; ++k) {
+                    const int64_t pos = (int64_t)mb * N + k;
+                    if (k >= N || pos >= prm.class_positions) continue;
+                    const float val = MODE == kModeF16x3 ? racc[k] * unscale : racc[k];
+                    if (prm.ksplit > 1) {
+                        const int ksi = (t >> 2) % prm.ksplit;
+                        prm.partial[((int64_t)(ksi * 4 + c) * prm.c_out + co) * prm.class_positions + pos] = val;
+                    } else {
+                        const int64_t b = pos / per;
+                        const int rem = (int)(pos - b * per);
+                        const int x = 2 * (rem / g.cols) + g.st_r, yy = 2 * (rem % g.cols) + g.st_s;
+                        reinterpret_cast<TY *>(prm.y)[(b * prm.c_out + co) * plane + (int64_t)x * prm.ow + yy] =
+                            cvt_out<TY>(val);
+                    }
                 }
             }
         }
@@ -329,7 +415,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             int c, mb, nb;
             decode(t, c, mb, nb);
             const ClassGeom &g = prm.cls[c];
-            const int nchunks = (g.R * g.C * prm.k_cblocks + CHUNK - 1) / CHUNK;
+            int k_lo, k_hi;
+            krange(t, k_lo, k_hi);
+            const int nchunks = (k_hi - k_lo + CHUNK - 1) / CHUNK;
             float racc[kTf32MaxN];
 #pragma unroll
             for (int k = 0; k < kTf32MaxN; ++k) racc[k] = 0.f;
@@ -351,7 +439,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
             const int64_t pos = (int64_t)mb * kBlockM + m;
-            if (pos < prm.class_positions) {
+            if (pos < prm.class_positions && prm.ksplit > 1) {  // split K: this range's fp32 partial
+                const int ksi = (t >> 2) % prm.ksplit;
+                float *pp = prm.partial + ((int64_t)(ksi * 4 + c) * prm.c_out + (int64_t)nb * N) * prm.class_positions + pos;
+                const int co_left = prm.c_out - nb * N;
+#pragma unroll
+                for (int k = 0; k < kTf32MaxN; ++k)
+                    if (k < N && k < co_left)
+                        pp[(int64_t)k * prm.class_positions] = MODE == kModeF16x3 ? racc[k] * unscale : racc[k];
+            } else if (pos < prm.class_positions) {
                 const int64_t per = (int64_t)g.rows * g.cols;
                 const int64_t b = pos / per;
                 const int rem = (int)(pos - b * per);
@@ -386,7 +482,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ch = 0; ch < N / 32; ++ch) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * N + ch * 32, v);
-                if (valid) {
+                if (valid && prm.ksplit > 1) {  // split K: this range's fp32 partial
+                    const int ksi = (t >> 2) % prm.ksplit;
+                    float *pp = prm.partial +
+                                ((int64_t)(ksi * 4 + c) * prm.c_out + (int64_t)nb * N + ch * 32) * prm.class_positions + pos;
+                    const int co_left = prm.c_out - nb * N - ch * 32;
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        if (k < co_left) pp[(int64_t)k * prm.class_positions] = __uint_as_float(v[k]);
+                } else if (valid) {
                     const int co_left = prm.c_out - nb * N - ch * 32;  // real channels in this chunk
                     if (co_left >= 32) {
 #pragma unroll
@@ -590,6 +694,29 @@ __global__ void nchw_to_nhwc_f16x2(const float *__restrict__ x, __half *__restri
     }
 }
 
+// Split-K reduction: every output element once, the ksplit partials of its class position summed
+// in ascending split order (a fixed order: bitwise reproducible), converted to the output type.
+template <typename TY>
+__global__ void splitk_reduce_kernel(const float *__restrict__ partial, TY *__restrict__ y, int ksplit, int c_out,
+                                     int oh, int ow, int rows, int cols, int swap, int64_t class_positions,
+                                     int64_t total) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int yy = (int)(e % ow);
+        const int64_t r1 = e / ow;
+        const int x = (int)(r1 % oh);
+        const int64_t r2 = r1 / oh;
+        const int co = (int)(r2 % c_out);
+        const int64_t b = r2 / c_out;
+        // output (x, y) belongs to class (r, s) = ((x + swap) & 1, (y + swap) & 1) at (x / 2, y / 2)
+        const int c = 2 * ((x + swap) & 1) + ((yy + swap) & 1);
+        const int64_t pos = (b * rows + (x >> 1)) * cols + (yy >> 1);
+        float acc = 0.f;
+        for (int ks = 0; ks < ksplit; ++ks)
+            acc += __ldcs(partial + ((int64_t)(ks * 4 + c) * c_out + co) * class_positions + pos);
+        y[e] = cvt_out<TY>(acc);
+    }
+}
+
 static int fp32_mode(const IgemmShape &s) {
     if (s.compute != SEGB_F32) return kModeBf16;
     return s.f16x3 ? kModeF16x3 : kModeTf32x3;
@@ -674,18 +801,43 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
         const int v = atoi(e);
         if (v >= 32 && v <= nmax && v % 32 == 0 && cop % v == 0) nt = v;
     }
-    if (nt % 32 || nt > nmax) return false;
+    // swapped operands (PM 3) for tiny batches: all class positions of the batch (16..128, a
+    // multiple of 16) as the N side of one tile, 128-channel weight blocks as the M side
+    const int64_t cpos = s.batch * (int64_t)rows * cols;
+    // (opt-in, SEGB200_K3_SWAP=1: correct, but measured slower than the narrow-N tiles on DCGAN l2/l3
+    // at batch 1 -- 53 vs 21 us for dcgan_l2 bf16 -- so tiny batches keep the output-stationary layout)
+    const char *swp = getenv("SEGB200_K3_SWAP");
+    if (mode != kModeTf32x3 && cpos <= kTf32MaxN && cpos % 16 == 0 && cop % kBlockM == 0 && rows * cols <= 256 &&
+        s.batch <= 256 && swp && atoi(swp)) {
+        prm.swap_ab = 1;
+        prm.box_w = cols; prm.box_h = rows; prm.box_b = (int)s.batch;
+        nt = (int)cpos;
+    }
+    if (!prm.swap_ab && (nt % 32 || nt > nmax)) return false;
     prm.n_tile = nt;
-    prm.n_blocks = cop / nt;
+    prm.n_blocks = prm.swap_ab ? cop / kBlockM : cop / nt;
     prm.batch = (int)s.batch; prm.c_in = s.c_in; prm.c_out = s.c_out; prm.oh = oh; prm.ow = ow; prm.p = p;
     const int kch = mode == kModeTf32x3 ? 32 : 64;
     prm.k_cblocks = (s.c_in + kch - 1) / kch;
     prm.class_positions = s.batch * (int64_t)rows * cols;
-    prm.m_tiles = (int)ceil_div(prm.class_positions, kBlockM);
+    prm.m_tiles = prm.swap_ab ? 1 : (int)ceil_div(prm.class_positions, kBlockM);
     prm.m_pairs = (prm.m_tiles + 1) / 2;
     const int64_t total = 4ll * prm.m_tiles * prm.n_blocks;
     if (total > INT32_MAX) return false;
     prm.total_tiles = (int)total;
+    // split K when the tiles cannot cover the SMs (small batches: a weight-streaming layer then runs
+    // on a handful of SMs); the partials are summed in a fixed order by splitk_reduce_kernel
+    prm.ksplit = 1;
+    {
+        const int nks = prm.cls[0].R * prm.cls[0].C * prm.k_cblocks;
+        if (total < 74 && nks >= 8)
+            prm.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>({8, nks / 4, ceil_div(148, total)}));
+        if (const char *e = getenv("SEGB200_K3_KSPLIT")) {  // A/B experiments
+            const int v = atoi(e);
+            if (v >= 1 && v <= 16 && v <= nks) prm.ksplit = v;
+        }
+        prm.total_tiles *= prm.ksplit;
+    }
     const int stage_bytes = (tf32 ? 2 : 1) * (kBlockM * 128 + nt * 128);
     prm.stages = std::min(8, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
     return prm.stages >= 2;
@@ -709,10 +861,15 @@ const char *igemm_kernel_name(const IgemmShape &s) {
                : s.c_in > 64         ? "K3b row-streaming GEMM (3xFP16, 64-channel passes)"
                                      : "K3b row-streaming GEMM (3xFP16)";
     const int mode = fp32_mode(s);
-    if (mode == kModeF16x3) return "K3 implicit GEMM (3xFP16)";
+    IgemmParams prm;
+    const bool sw = make_params(s, prm) && prm.swap_ab, split = prm.ksplit > 1;
+    if (mode == kModeF16x3)
+        return sw ? (split ? "K3 implicit GEMM (3xFP16, swapped operands, split K)" : "K3 implicit GEMM (3xFP16, swapped operands)")
+                  : (split ? "K3 implicit GEMM (3xFP16, split K)" : "K3 implicit GEMM (3xFP16)");
     if (mode == kModeTf32x3) return "K3 implicit GEMM (3xTF32)";
     if (igemm_cp_supported(s)) return "K3p class-pair GEMM (bf16)";
-    return "K3 implicit GEMM (bf16)";
+    return sw ? (split ? "K3 implicit GEMM (bf16, swapped operands, split K)" : "K3 implicit GEMM (bf16, swapped operands)")
+              : (split ? "K3 implicit GEMM (bf16, split K)" : "K3 implicit GEMM (bf16)");
 }
 
 // K3's only workspace: the channels-last A operand (bf16, or fp32 hi followed by fp32 lo for
@@ -724,7 +881,12 @@ int64_t igemm_workspace_bytes(const IgemmShape &s) {
     const int mode = fp32_mode(s);
     const int64_t elems = s.batch * (int64_t)s.c_in * s.h * s.w;
     const int64_t bpe = mode == kModeTf32x3 ? 8 : (mode == kModeF16x3 ? 4 : 2);  // bytes per element, all planes
-    return (elems * bpe + 255) / 256 * 256 + (mode == kModeF16x3 ? kAbsmaxBytes : 0);  // + the absmax partials
+    IgemmParams prm;
+    int64_t split = 0;  // split K: fp32 partials of every class position and channel per split
+    if (make_params(s, prm) && prm.ksplit > 1)
+        split = ((int64_t)prm.ksplit * 4 * s.c_out * prm.class_positions * 4 + 255) / 256 * 256;
+    // the A planes, the absmax partials, the split-K partials
+    return (elems * bpe + 255) / 256 * 256 + (mode == kModeF16x3 ? kAbsmaxBytes : 0) + split;
 }
 
 static int encode_map(CUtensorMap *m, CUtensorMapDataType dt, int rank, const void *ptr, const cuuint64_t *dims,
@@ -741,7 +903,7 @@ static int launch_k3(unsigned grid, size_t smem, cudaStream_t st, const CUtensor
                      const CUtensorMap &tmAlo, const CUtensorMap &tmBlo, const IgemmParams &prm) {
     auto kern = igemm_tconv_kernel<TY, MODE, PM>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (PM == 0) {
+    if (PM == 0 || PM == 3) {
         kern<<<grid, kThreads, smem, st>>>(tmA, tmB, tmAlo, tmBlo, prm);
         return SEGB_OK;
     }
@@ -833,14 +995,22 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     const char *pm_env = getenv("SEGB200_K3_PAIR");
     int pm = pm_env ? std::max(0, std::min(2, atoi(pm_env))) : 2;
     if (prm.m_tiles < 2) pm = 0;
-    const bool pair = pm > 0;
-    if (pair) prm.total_tiles = 4 * prm.m_pairs * prm.n_blocks;
+    if (prm.swap_ab) pm = 3;
+    const bool pair = pm == 1 || pm == 2;
+    if (pair) prm.total_tiles = 4 * prm.m_pairs * prm.n_blocks * prm.ksplit;
+    {
+        const int64_t bpe = mode == kModeTf32x3 ? 8 : (mode == kModeF16x3 ? 4 : 2);  // all A planes
+        prm.partial = prm.ksplit > 1 ? (float *)((char *)ws + (elems * bpe + 255) / 256 * 256 +
+                                                (mode == kModeF16x3 ? kAbsmaxBytes : 0))
+                                     : nullptr;
+    }
     {  // stages: TWO holds only half of the B tile per CTA
         const int b_cta = (pm == 2 ? prm.n_tile / 2 : prm.n_tile) * 128;
         const int stage_bytes = (tf32 ? 2 : 1) * (kBlockM * 128 + b_cta);
         prm.stages = std::min(8, (int)((227 * 1024 - 1024 - 256) / stage_bytes));
     }
-    cuuint32_t bbox[3] = {(cuuint32_t)kch, (cuuint32_t)(pair ? prm.n_tile / 2 : prm.n_tile), 1};
+    cuuint32_t bbox[3] = {(cuuint32_t)kch,
+                          (cuuint32_t)(prm.swap_ab ? kBlockM : (pair ? prm.n_tile / 2 : prm.n_tile)), 1};
     int rc = encode_map(&tmA, dt, 4, xs, adims, astr, abox, "A");
     if (!rc) rc = encode_map(&tmB, dt, 3, wg, bdims, bstr, bbox, "B");
     if (!rc && tf32) rc = encode_map(&tmAlo, dt, 4, xs_lo, adims, astr, abox, "A lo");
@@ -859,7 +1029,8 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     const unsigned grid = pair ? 2 * (unsigned)std::min<int64_t>(prm.total_tiles, sms / 2)
                                : (unsigned)std::min<int64_t>(prm.total_tiles, sms);
 #define SEGB_K3_LAUNCH(TY_, TF_)                                                                       \
-    rc = pm == 2   ? launch_k3<TY_, TF_, 2>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
+    rc = pm == 3   ? launch_k3<TY_, TF_, 3>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
+         : pm == 2 ? launch_k3<TY_, TF_, 2>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
          : pm == 1 ? launch_k3<TY_, TF_, 1>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm)                \
                    : launch_k3<TY_, TF_, 0>(grid, smem, st, tmA, tmB, tmAlo, tmBlo, prm);
     if (mode == kModeF16x3) {
@@ -874,7 +1045,22 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
 #undef SEGB_K3_LAUNCH
     if (rc) return rc;
     note_launch();
-    return check_launch("igemm_tconv_kernel");
+    if (int e = check_launch("igemm_tconv_kernel")) return e;
+    if (prm.ksplit > 1) {
+        const int64_t total = s.batch * (int64_t)s.c_out * prm.oh * prm.ow;
+        const unsigned g = (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+        const ClassGeom &g0 = prm.cls[0];
+        if (s.y_dtype == SEGB_BF16)
+            splitk_reduce_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(prm.partial, (__nv_bfloat16 *)y, prm.ksplit,
+                                                                   s.c_out, prm.oh, prm.ow, g0.rows, g0.cols,
+                                                                   s.pad & 1, prm.class_positions, total);
+        else
+            splitk_reduce_kernel<float><<<g, 256, 0, st>>>(prm.partial, (float *)y, prm.ksplit, s.c_out, prm.oh, prm.ow,
+                                                           g0.rows, g0.cols, s.pad & 1, prm.class_positions, total);
+        note_launch();
+        return check_launch("splitk_reduce_kernel");
+    }
+    return SEGB_OK;
 }
 
 }  // namespace segb
