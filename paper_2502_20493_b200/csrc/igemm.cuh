@@ -36,6 +36,7 @@ int run_igemm_cp_core(const IgemmShape &s, const void *x_nhwc, const void *wg, v
 
 // K3b: row-streaming variant for wide class grids (igemm_rows_sm100.cu)
 bool igemm_rows_supported(const IgemmShape &s);
+int igemm_rows_variant(const IgemmShape &s);  // its CTA split (3 / 4: 2-SM pairs), 0 if unsupported
 int64_t igemm_rows_workspace_bytes(const IgemmShape &s);  // 3xFP16: the input's absmax partials
 int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, const void *wg_lo, void *y, void *ws,
                    int64_t ws_bytes, cudaStream_t st);

@@ -375,7 +375,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // 2i+1 run and the next tile's first half can start as soon as a half buffer is free
     constexpr bool HALF = RS == 5;
     constexpr int NCL = (RS == 2 || HALF) ? 2 : 4;  // parity classes per accumulator buffer
-    constexpr int NBUF = (HALF || F16) ? 4 : 2;     // TMEM accumulator buffers (F16: deeper, 64-position tiles)
+#ifndef SEGB_ROWS_PAIR_NBUF
+#define SEGB_ROWS_PAIR_NBUF 2
+#endif
+    // TMEM accumulator buffers: F16 (64-position tiles) keeps 4; the bf16 pair (RS 3) is an A/B knob
+    constexpr int NBUF = (HALF || F16) ? 4 : (RS == 3 ? SEGB_ROWS_PAIR_NBUF : 2);
     // M = 64 rows with two channel blocks: loader warps 0-1 fill block 0, warps 2-3 block 1 of
     // the same input row at once (else each unit is one (row, block) filled by all four)
     constexpr bool PAIRKB = MR == 64 && KBC == 2;
@@ -800,6 +804,28 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         int bkb[kLoadBufs];     // channel block of the unit in each buffer
         bool bv[kLoadBufs];     // buffer holds a unit
         int ct = t0, cl = t0 < t1 ? nr - loads_of(t0) : 0, ckb_ = 0;  // next unit to load
+        // L2 prefetch of the unit kBfPrefetch units beyond the register loads (one 128-byte line of
+        // its row segment per thread: 64 channels x MR columns x 2 B)
+#ifndef SEGB_ROWS_BF16_PREFETCH
+#define SEGB_ROWS_BF16_PREFETCH 0
+#endif
+        constexpr int kBfPrefetch = SEGB_ROWS_BF16_PREFETCH;
+        int pt = ct, pl = cl, pkb = ckb_;
+        auto prefetch_unit = [&]() {
+            if (pt >= t1) return;
+            const int ta = pt + toff;
+            const int i = ta % prm.rows, rest = ta / prm.rows;
+            const int ms = rest % prm.msub, b = rest / prm.msub;
+            const int row = i + dminr + pl;
+            if (row < 0 || row >= prm.h) return;
+            constexpr int LPC = MR * 2 / 128;  // lines per channel row segment
+            const int ch = (PAIRKB ? kbt * 64 : pkb * 64) + tt / LPC;
+            if (tt >= 64 * LPC || ch >= prm.c_in) return;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(x + ((int64_t)b * prm.c_in + ch) * plane_in +
+                                                        (int64_t)row * prm.w + ms * MR + (tt % LPC) * 64));
+        };
+        if (kBfPrefetch > 0)
+            for (int k = 0; k < kLoadBufs + kBfPrefetch && pt < t1; ++k) advance(pt, pl, pkb);
 #pragma unroll
         for (int k = 0; k < kLoadBufs; ++k) {
             bv[k] = ct < t1;
@@ -864,6 +890,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (bv[k]) {
                     load_unit(ct, cl, ckb_, rb[k], hb[k]);
                     advance(ct, cl, ckb_);
+                    if (kBfPrefetch > 0) {
+                        prefetch_unit();
+                        advance(pt, pl, pkb);
+                    }
                 }
             }
         }
@@ -1216,6 +1246,12 @@ static bool rows_instantiated(int nh, int kbc, int swap, int mr, int nsplit, boo
     if (mr == 128 && nsplit == 2) return nh == 2 && kbc == 2 && swap == 0;
     if (mr == 64 && nh == 2 && swap == 0) return true;
     return mr == 64 && nh == 2 && kbc == 2 && swap == 1 && nsplit == 2;
+}
+
+int igemm_rows_variant(const IgemmShape &s) {
+    RowsParams prm;
+    int nh, kbc, swap, mr, nsplit;
+    return rows_params(s, prm, nh, kbc, swap, mr, nsplit) ? nsplit : 0;
 }
 
 bool igemm_rows_supported(const IgemmShape &s) {

@@ -855,21 +855,32 @@ bool igemm_supported(const IgemmShape &s) {
 }
 
 const char *igemm_kernel_name(const IgemmShape &s) {
+    // the family, the operand mode and the tile configuration (a different N tile, split or pair
+    // layout changes the summation bits, so the name says which one ran)
+    static thread_local std::string name;
+    char buf[160];
     if (igemm_scatter_supported(s)) return "K3c scatter-GEMM + gather (bf16)";
-    if (use_rows(s))
-        return s.compute != SEGB_F32 ? "K3b row-streaming GEMM (bf16)"
-               : s.c_in > 64         ? "K3b row-streaming GEMM (3xFP16, 64-channel passes)"
-                                     : "K3b row-streaming GEMM (3xFP16)";
+    if (use_rows(s)) {
+        const int ns = igemm_rows_variant(s);
+        snprintf(buf, sizeof buf, "K3b row-streaming GEMM (%s%s)%s", s.compute != SEGB_F32 ? "bf16" : "3xFP16",
+                 s.compute == SEGB_F32 && s.c_in > 64 ? ", 64-channel passes" : "",
+                 ns == 3 || ns == 4 ? " [2-SM pairs]" : ns == 2 ? " [row-parity CTA pairs]" : "");
+        name = buf;
+        return name.c_str();
+    }
     const int mode = fp32_mode(s);
+    if (mode == kModeBf16 && igemm_cp_supported(s)) return "K3p class-pair GEMM (bf16)";
     IgemmParams prm;
-    const bool sw = make_params(s, prm) && prm.swap_ab, split = prm.ksplit > 1;
-    if (mode == kModeF16x3)
-        return sw ? (split ? "K3 implicit GEMM (3xFP16, swapped operands, split K)" : "K3 implicit GEMM (3xFP16, swapped operands)")
-                  : (split ? "K3 implicit GEMM (3xFP16, split K)" : "K3 implicit GEMM (3xFP16)");
-    if (mode == kModeTf32x3) return "K3 implicit GEMM (3xTF32)";
-    if (igemm_cp_supported(s)) return "K3p class-pair GEMM (bf16)";
-    return sw ? (split ? "K3 implicit GEMM (bf16, swapped operands, split K)" : "K3 implicit GEMM (bf16, swapped operands)")
-              : (split ? "K3 implicit GEMM (bf16, split K)" : "K3 implicit GEMM (bf16)");
+    if (!make_params(s, prm)) return "K3 implicit GEMM (unsupported shape)";
+    const char *pm_env = getenv("SEGB200_K3_PAIR");
+    const int pm = prm.swap_ab ? 3 : prm.m_tiles < 2 ? 0 : pm_env ? std::max(0, std::min(2, atoi(pm_env))) : 2;
+    snprintf(buf, sizeof buf, "K3 implicit GEMM (%s%s) [N %d%s%s]",
+             mode == kModeF16x3 ? "3xFP16" : mode == kModeTf32x3 ? "3xTF32" : "bf16",
+             prm.swap_ab ? ", swapped operands" : "", prm.n_tile,
+             pm == 2 ? ", 2-SM pairs" : pm == 1 ? ", multicast pairs" : "",
+             prm.ksplit > 1 ? (std::string(", split K ") + std::to_string(prm.ksplit)).c_str() : "");
+    name = buf;
+    return name.c_str();
 }
 
 // K3's only workspace: the channels-last A operand (bf16, or fp32 hi followed by fp32 lo for
