@@ -806,8 +806,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         int ct = t0, cl = t0 < t1 ? nr - loads_of(t0) : 0, ckb_ = 0;  // next unit to load
         // L2 prefetch of the unit kBfPrefetch units beyond the register loads (one 128-byte line of
         // its row segment per thread: 64 channels x MR columns x 2 B)
+        // (measured: 128-wide single-CTA rows, ebgan_l7 0.608 -> 0.575 ms; the 2-SM pair, l6, +2%: off)
 #ifndef SEGB_ROWS_BF16_PREFETCH
-#define SEGB_ROWS_BF16_PREFETCH 0
+#define SEGB_ROWS_BF16_PREFETCH ((RS == 1 && MR == 128) ? 4 : 0)
 #endif
         constexpr int kBfPrefetch = SEGB_ROWS_BF16_PREFETCH;
         int pt = ct, pl = cl, pkb = ckb_;
