@@ -51,6 +51,11 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kLoaderWarp0 = 8;                               // first of the 4 row-loader warps
 constexpr int kRowsThreads = 12 * 32;                         // launch budget: 168 registers
 constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168 + 232) <= 64 K
+// 3xFP16: the epilogue holds a whole tile's accumulators (4 classes x 32 columns) at once
+#ifndef SEGB_ROWS_F16_ST16  // 3xFP16 epilogue stores: 16-byte (lane-pair exchange) or two 8-byte per channel
+#define SEGB_ROWS_F16_ST16 0  // measured: 8-byte stores without exchange -3.5% (l7), -8% (l6) vs 16-byte
+#endif
+constexpr int kRegsLoadF16 = 192, kRegsEpiF16 = 216;          // 128 x (96 + 216 + 192) <= 128 x 3 x 168
 constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
 #ifndef SEGB_ROWS_LOAD_BUFS
 #define SEGB_ROWS_LOAD_BUFS 3
@@ -562,7 +567,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }  // warps 2, 3: idle (they only take part in warpgroup 0's register release)
     } else if (warp >= kLoaderWarp0) {
 #ifndef SEGB_ROWS_NO_SETMAXNREG
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsLoad));
+        // (3xFP16: the loaders hold 3 x 32 fp32 registers of units; the epilogue gets the rest)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(F16 ? kRegsLoadF16 : kRegsLoad));
 #endif
         // ---------------- row loaders / transposers: NCHW input row (64 channels x MR columns
         // + halo) -> K-major SWIZZLE_128B slot rows. Thread (cg = t & 7, cc = t >> 3) loads 8
@@ -692,7 +698,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         break;
                     }
                     const int sidx = qs;
+                    long long pl_ = clock64();
+                    if (tw == 0) { ROWS_PROF(7, pl_) }
                     if (!(ABL(64))) mbar_wait(&slot_empty[sidx], qph ^ 1);
+                    if (tw == 0) { ROWS_PROF(6, pl_) }
                     const uint32_t dst = smem_u32(sRing + sidx * prm.slot_bytes);
                     if (!(ABL(16))) {
                         uint32_t hp[8][2], lp[8][2];  // [channel][q]: columns 2q, 2q+1 as fp16 pairs
@@ -900,6 +909,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         }
     } else {
+#ifndef SEGB_ROWS_NO_SETMAXNREG
+        if constexpr (F16) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpiF16));
+#endif
         // ---------------- epilogue (warps 4..7): warp reads TMEM lane quarter warp % 4. The
         // classes of a position are in registers, so each lane writes the pair of output
         // columns (2j, 2j+1) of each of its output rows as one 4-byte bf16x2 store: a warp
@@ -960,20 +972,27 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)r * prm.ow + h * 32));
             };
             if (prm.accumulate && t0 < t1) prefetch_tile(t0);
+            // the tile's (row i, segment ms, sample b), advanced incrementally (no per-tile divisions)
+            int ei = (t0 + toff) % prm.rows, ems = ((t0 + toff) / prm.rows) % prm.msub,
+                eb = ((t0 + toff) / prm.rows) / prm.msub;
             for (int t = t0; t < t1; ++t) {
-                const int ta = t + toff;
-                const int i = ta % prm.rows, rest = ta / prm.rows;
-                const int ms = rest % prm.msub, b = rest / prm.msub;
+                const int i = ei, ms = ems, b = eb;
+                if (++ei == prm.rows) {
+                    ei = 0;
+                    if (++ems == prm.msub) { ems = 0; ++eb; }
+                }
                 if (prm.accumulate && t + 1 < t1) prefetch_tile(t + 1);
+                long long pe_ = clock64();
+                if (warp == kEpiWarp0) { ROWS_PROF(4, pe_) }
                 if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
+                if (warp == kEpiWarp0) { ROWS_PROF(3, pe_) }
                 tc_fence_after();
                 const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NCL * NE;
                 float *pf = reinterpret_cast<float *>(prm.y) + ((int64_t)b * prm.c_out + chalf * NE) * plane +
                             (int64_t)(2 * i + row_off) * prm.ow + (int64_t)ms * 2 * MR + 2 * m;
                 const int odd = lane & 1;
                 float *pf4 = pf - 2 * odd + odd * prm.ow;  // even lane: row 2i, col 2m; odd: row 2i+1, col 2m-2
-                constexpr int CH = kEpiChunk;
-                uint32_t v[NCL][CH], v2[NCL][CH];
+                (void)pf4;
                 if (ABL(8)) {  // ablation: no TMEM reads (nor stores)
                     tc_fence_before();
                     __syncwarp();
@@ -981,6 +1000,89 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
                     continue;
                 }
+#ifndef SEGB_ROWS_F16_EPI_WHOLE
+#define SEGB_ROWS_F16_EPI_WHOLE 1
+#endif
+#if SEGB_ROWS_F16_EPI_WHOLE
+                {  // (F16: c_out <= 64 split over the pair, so NE <= 32)
+                    // the whole tile's accumulators in one go (4 classes x NE columns, one wait), the
+                    // TMEM buffer released before any store: the MMAs of the next tiles do not wait
+                    // for this tile's output writes
+                    uint32_t va[NCL][32];
+#pragma unroll
+                    for (int c = 0; c < NCL; ++c) {
+                        tmem_ld16(tl + c * NE, *reinterpret_cast<uint32_t(*)[16]>(&va[c][0]));
+                        if (NE > 16) tmem_ld16(tl + c * NE + 16, *reinterpret_cast<uint32_t(*)[16]>(&va[c][16]));
+                    }
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < NCL; ++c)
+#pragma unroll
+                        for (int k = 0; k < 32; k += 8) reg_fence8(*reinterpret_cast<uint32_t(*)[8]>(&va[c][k]));
+                    tc_fence_before();
+                    __syncwarp();
+                    // relaxed: the accumulators are in registers (waited); a release would first wait
+                    // for the previous tile's global stores (ncu: 91% membar stalls on that arrive)
+#ifndef SEGB_ROWS_F16_RELEASE_ARRIVE
+                    if (lane == 0) {
+                        if (TWO) mbar_arrive_relaxed_cluster(mapa_rank(&tempty[acc], 0));
+                        else mbar_arrive_relaxed(&tempty[acc]);
+                    }
+#else
+                    if (lane == 0) release_acc(acc);
+#endif
+#pragma unroll
+                    for (int g8 = 0; g8 < 32; g8 += 8) {
+                        if (g8 >= NE) break;
+                        float4 old[8];
+                        if (prm.accumulate && lane_active) {
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+#if SEGB_ROWS_F16_ST16
+                                old[k] = __ldcs(reinterpret_cast<const float4 *>(pf4 + (int64_t)(g8 + k) * plane));
+#else
+                                const float2 o0 = __ldcs(reinterpret_cast<const float2 *>(pf + (int64_t)(g8 + k) * plane));
+                                const float2 o1 =
+                                    __ldcs(reinterpret_cast<const float2 *>(pf + (int64_t)(g8 + k) * plane + prm.ow));
+                                old[k] = make_float4(o0.x, o0.y, o1.x, o1.y);
+#endif
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int co = g8 + k;
+                            const float2 r0 = make_float2(__uint_as_float(va[C00][co]) * us, __uint_as_float(va[C01][co]) * us);
+                            const float2 r1 = make_float2(__uint_as_float(va[C10][co]) * us, __uint_as_float(va[C11][co]) * us);
+#if SEGB_ROWS_F16_ST16
+                            const float2 give = odd ? r0 : r1;
+                            const float2 got = make_float2(__shfl_xor_sync(0xffffffffu, give.x, 1),
+                                                           __shfl_xor_sync(0xffffffffu, give.y, 1));
+                            float4 v4 = odd ? make_float4(got.x, got.y, r1.x, r1.y) : make_float4(r0.x, r0.y, got.x, got.y);
+                            if (lane_active && !(ABL(1))) {
+                                if (prm.accumulate)
+                                    v4 = make_float4(old[k].x + v4.x, old[k].y + v4.y, old[k].z + v4.z, old[k].w + v4.w);
+                                *reinterpret_cast<float4 *>(pf4 + (int64_t)co * plane) = v4;
+                            }
+#else  // two 8-byte stores per channel, no lane exchange (old values as two float2 in old[k])
+                            if (lane_active && !(ABL(1))) {
+                                float2 *d0 = reinterpret_cast<float2 *>(pf + (int64_t)co * plane);
+                                float2 a0 = r0, a1 = r1;
+                                if (prm.accumulate) {
+                                    a0 = make_float2(old[k].x + r0.x, old[k].y + r0.y);
+                                    a1 = make_float2(old[k].z + r1.x, old[k].w + r1.y);
+                                }
+                                d0[0] = a0;
+                                *reinterpret_cast<float2 *>(pf + (int64_t)co * plane + prm.ow) = a1;
+                            }
+#endif
+                        }
+                    }
+                    if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+                    continue;
+                }
+#else
+                constexpr int CH = kEpiChunk;
+                uint32_t v[NCL][CH], v2[NCL][CH];
 #pragma unroll
                 for (int c = 0; c < NCL; ++c) tmem_ld_chunk(tl + c * NE, v[c]);
                 auto chunk = [&](int co0, uint32_t (&cur)[NCL][CH], uint32_t (&nxt)[NCL][CH]) {
@@ -1030,6 +1132,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     if (co0 + CH < NE) chunk(co0 + CH, v2, v);
                 }
                 if (++acc == NBUF) { acc = 0; acc_phase ^= 1; }
+#endif
             }
         } else
         for (int u = t0 * HT; u < t1 * HT; ++u) {
