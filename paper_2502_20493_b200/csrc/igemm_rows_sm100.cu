@@ -57,6 +57,21 @@ constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168
 #endif
 constexpr int kRegsLoadF16 = 192, kRegsEpiF16 = 216;          // 128 x (96 + 216 + 192) <= 128 x 3 x 168
 constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
+// 3xFP16 loaders hand each filled slot to an "arriver" warp (warp 2) through a named barrier;
+// the arriver's cluster-scope release arrive then has no outstanding global loads to wait for
+// (a release arrive from a loader lane waited for the next units' loads in flight: 1850 cycles
+// per unit on ebgan_l7, and the register pipelining of the loads collapsed to one unit)
+#ifndef SEGB_ROWS_ARRIVER
+#define SEGB_ROWS_ARRIVER 1
+#endif
+// (loaders and arriver both bar.sync on named barrier 1; measured: loaders that only bar.arrive on
+// one barrier per slot, not waiting for the arriver, +1.5% on ebgan_l7)
+constexpr int kArriverWarp = 2;
+constexpr int kSlotBar0 = 1;
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 #ifndef SEGB_ROWS_LOAD_BUFS
 #define SEGB_ROWS_LOAD_BUFS 3
 #endif
@@ -417,7 +432,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(b_full, HALF ? 2 : 1);  // HALF: the two schedules' weights, two expect_tx
         for (int i = 0; i < ring * KBC; ++i) {
-            mbar_init(&slot_full[i], (PAIRKB ? 2 : 4) * CG);  // one arrival per loader warp filling the slot
+            // one arrival per loader warp filling the slot (3xFP16 with the arriver: one per CTA)
+            mbar_init(&slot_full[i], ((F16 && SEGB_ROWS_ARRIVER) ? 1 : PAIRKB ? 2 : 4) * CG);
             mbar_init(&slot_empty[i], 1);
         }
         for (int i = 0; i < NBUF; ++i) {
@@ -564,7 +580,21 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (!HALF && ++acc == NBUF) { acc = 0; acc_phase ^= 1; }
             }
             }
-        }  // warps 2, 3: idle (they only take part in warpgroup 0's register release)
+        } else if (F16 && SEGB_ROWS_ARRIVER && warp == kArriverWarp) {
+            // ---------------- the arriver: one slot_full arrival per unit the loaders filled, in
+            // the loaders' unit order (tile t adds loads_of(t) rows)
+            uint32_t qs = 0;
+            for (int t = t0; t < t1; ++t)
+                for (int l = loads_of(t); l > 0; --l) {
+                    named_bar_sync(kSlotBar0, 32 * 5);
+                    if (lane == 0 && !(ABL(64))) {
+                        if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[qs], 0));
+                        else mbar_arrive(&slot_full[qs]);
+                    }
+                    __syncwarp();
+                    if (++qs == (uint32_t)ring) qs = 0;
+                }
+        }  // warps 2 (unless the arriver), 3: idle (they only take part in warpgroup 0's register release)
     } else if (warp >= kLoaderWarp0) {
 #ifndef SEGB_ROWS_NO_SETMAXNREG
         // (3xFP16: the loaders hold 3 x 32 fp32 registers of units; the epilogue gets the rest)
@@ -690,6 +720,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
             uint32_t qs = 0, qph = 0;
             bool more = bv[0];
+            long long pl_ = clock64();
             while (more) {
 #pragma unroll
                 for (int k = 0; k < KLB; ++k) {
@@ -698,7 +729,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         break;
                     }
                     const int sidx = qs;
-                    long long pl_ = clock64();
                     if (tw == 0) { ROWS_PROF(7, pl_) }
                     if (!(ABL(64))) mbar_wait(&slot_empty[sidx], qph ^ 1);
                     if (tw == 0) { ROWS_PROF(6, pl_) }
@@ -751,12 +781,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                                      "r"(ol[0]), "r"(ol[1]), "r"(ol[2]), "r"(ol[3])
                                      : "memory");
                     }
+                    if (tw == 0) { ROWS_PROF(12, pl_) }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0 && !(ABL(64))) {
+                    if (tw == 0) { ROWS_PROF(14, pl_) }
+                    if constexpr (SEGB_ROWS_ARRIVER) {
+                        named_bar_sync(kSlotBar0, 32 * 5);
+                    } else if (lane == 0 && !(ABL(64))) {
                         if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));
                         else mbar_arrive(&slot_full[sidx]);
                     }
+                    if (tw == 0) { ROWS_PROF(13, pl_) }
                     if (++qs == (uint32_t)ring) { qs = 0; qph ^= 1; }
                     bv[k] = cu.t < t1;
                     if (bv[k]) {

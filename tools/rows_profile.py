@@ -24,6 +24,7 @@ buf = (ctypes.c_ulonglong * 16)()
 _lib.lib().segb_debug_rows_profile(buf)
 v = list(buf)
 names = ["mma wait tempty", "mma wait slots", "mma issue", "epi wait tfull", "epi work", "epi tma-issue",
-         "loader wait empty", "loader work", "-", "epi bulk wait", "epi sts", "epi fence"]
+         "loader wait empty", "loader work", "-", "epi bulk wait", "epi sts", "epi fence",
+         "loader convert+sts", "loader arrive", "loader fence"]
 for k, nm in enumerate(names):
     print(f"{nm:18s} {v[k]:>12d}")
