@@ -66,6 +66,9 @@ constexpr int kRingMax = 8;         // input-row slots: as many as shared memory
 #endif
 // (loaders and arriver both bar.sync on named barrier 1; measured: loaders that only bar.arrive on
 // one barrier per slot, not waiting for the arriver, +1.5% on ebgan_l7)
+#ifndef SEGB_ROWS_ARRIVER_BF16  // the same for the bf16 loaders (M = 64 pairs: one barrier per channel-block half)
+#define SEGB_ROWS_ARRIVER_BF16 1
+#endif
 constexpr int kArriverWarp = 2;
 constexpr int kSlotBar0 = 1;
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // the same input row at once (else each unit is one (row, block) filled by all four)
     constexpr bool PAIRKB = MR == 64 && KBC == 2;
     constexpr int UKB = PAIRKB ? 1 : KBC;  // channel blocks iterated per row by a loader thread
+    constexpr bool ARR = F16 ? SEGB_ROWS_ARRIVER : SEGB_ROWS_ARRIVER_BF16;  // slot hand-off via warp 2
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int rsel = RS == 2 ? (int)(blockIdx.x % 2) : -1;
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         mbar_init(b_full, HALF ? 2 : 1);  // HALF: the two schedules' weights, two expect_tx
         for (int i = 0; i < ring * KBC; ++i) {
             // one arrival per loader warp filling the slot (3xFP16 with the arriver: one per CTA)
-            mbar_init(&slot_full[i], ((F16 && SEGB_ROWS_ARRIVER) ? 1 : PAIRKB ? 2 : 4) * CG);
+            mbar_init(&slot_full[i], (ARR ? 1 : PAIRKB ? 2 : 4) * CG);
             mbar_init(&slot_empty[i], 1);
         }
         for (int i = 0; i < NBUF; ++i) {
@@ -580,18 +584,24 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 if (!HALF && ++acc == NBUF) { acc = 0; acc_phase ^= 1; }
             }
             }
-        } else if (F16 && SEGB_ROWS_ARRIVER && warp == kArriverWarp) {
+        } else if (ARR && warp == kArriverWarp) {
             // ---------------- the arriver: one slot_full arrival per unit the loaders filled, in
-            // the loaders' unit order (tile t adds loads_of(t) rows)
+            // the loaders' unit order (tile t adds loads_of(t) rows, each of KBC channel blocks;
+            // M = 64 pairs: the two blocks of a row are filled at once by loader warps 0-1 / 2-3,
+            // each half on its own barrier)
             uint32_t qs = 0;
             for (int t = t0; t < t1; ++t)
                 for (int l = loads_of(t); l > 0; --l) {
-                    named_bar_sync(kSlotBar0, 32 * 5);
-                    if (lane == 0 && !(ABL(64))) {
-                        if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[qs], 0));
-                        else mbar_arrive(&slot_full[qs]);
+#pragma unroll
+                    for (int kb = 0; kb < KBC; ++kb) {
+                        if (PAIRKB) named_bar_sync(kSlotBar0 + kb, 32 * 3);
+                        else named_bar_sync(kSlotBar0, 32 * 5);
+                        if (lane == 0 && !(ABL(64))) {
+                            if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[qs * KBC + kb], 0));
+                            else mbar_arrive(&slot_full[qs * KBC + kb]);
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
                     if (++qs == (uint32_t)ring) qs = 0;
                 }
         }  // warps 2 (unless the arriver), 3: idle (they only take part in warpgroup 0's register release)
@@ -785,7 +795,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (tw == 0) { ROWS_PROF(14, pl_) }
-                    if constexpr (SEGB_ROWS_ARRIVER) {
+                    if constexpr (ARR) {
                         named_bar_sync(kSlotBar0, 32 * 5);
                     } else if (lane == 0 && !(ABL(64))) {
                         if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));
@@ -922,7 +932,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                 }
                 fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
                 __syncwarp();
-                if (lane == 0 && !(ABL(64))) {
+                if constexpr (ARR) {
+                    if (PAIRKB) named_bar_sync(kSlotBar0 + kbt, 32 * 3);
+                    else named_bar_sync(kSlotBar0, 32 * 5);
+                } else if (lane == 0 && !(ABL(64))) {
                     if (TWO) mbar_arrive_cluster(mapa_rank(&slot_full[sidx], 0));  // the leader's barrier
                     else mbar_arrive(&slot_full[sidx]);
                 }
