@@ -1,6 +1,7 @@
 // The C ABI (include/segb200.h): validation with the reference's error
 // taxonomy, the prepared-layer object, and kernel dispatch.
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "direct_impl.cuh"
@@ -77,6 +78,7 @@ struct segb_layer {
     void *wz = nullptr;  // K3c weights (bf16, (kx, ky, co) rows x 64-padded c_in, K-major)
     void *ws = nullptr;  // workspace reserved by segb_layer_reserve_workspace (segb_forward)
     int64_t ws_bytes = 0;
+    std::vector<float> w_pair;  // K2p: host copy of the fp32 K2 weights (a kernel parameter), or empty
 };
 
 namespace segb {
@@ -339,6 +341,14 @@ int segb_prepare(const void *bank, int bank_dtype, int c_in, int c_out, int n, i
     if (!rc && compute == SEGB_BF16 && may_use_scatter(L)) rc = ensure_scatter_weights(L, false, st);
     if (!rc && compute == SEGB_F32 && may_use_f16x3(L) && !want_tf32x3()) rc = ensure_f16x3_weights(L, false, st);
     if (!rc && compute == SEGB_F32 && may_use_tf32(L) && !L->wf) rc = ensure_tf32_weights(L, false, st);
+    if (!rc && compute == SEGB_F32 && engine == SEGB_ENGINE_SEGREGATED && direct_pair_ok(c_in, c_out, n, L->n2p)) {
+        // K2p takes its (few) weights as a kernel parameter: one host copy, made here
+        L->w_pair.resize((size_t)c_in * c_out * L->n2p);
+        cudaError_t e2 = cudaMemcpyAsync(L->w_pair.data(), L->wd[SEGB_F32], L->w_pair.size() * sizeof(float),
+                                         cudaMemcpyDeviceToHost, st);
+        if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(st);
+        if (e2 != cudaSuccess) rc = fail(SEGB_ERR_CUDA, "paired direct-kernel weights: %s", cudaGetErrorString(e2));
+    }
     if (rc) {
         segb_release(L);
         return rc;
@@ -414,6 +424,15 @@ static int plan_forward(const segb_layer *L, int x_dtype, int64_t batch, int in_
     return SEGB_OK;
 }
 
+// K2p for the direct path: fp32 compute on f32 / u8-image x into f32 y, the layer's host weight
+// copy made at prepare (SEGB200_DIRECT_PAIR=0 keeps K2, for A/B runs and the bitwise test)
+static bool use_direct_pair(const segb_layer *L, int x_dtype, int y_dtype, int compute) {
+    if (L->w_pair.empty() || compute != SEGB_F32 || y_dtype != SEGB_F32) return false;
+    if (x_dtype != SEGB_F32 && x_dtype != SEGB_U8_HWC) return false;
+    const char *e = getenv("SEGB200_DIRECT_PAIR");
+    return !(e && !atoi(e));
+}
+
 static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
                         int y_dtype, int compute, int path, void *ws, int64_t ws_bytes, cudaStream_t st) {
     FwdPlan pl;
@@ -451,6 +470,9 @@ static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch
     a.nqc = (ow - 1 + a.swap) / 2 + 1;
     const bool ref = L->engine == SEGB_ENGINE_REFERENCE;
     if (ref) a.p = L->pad;  // the reference engine pads the upsampled map by P
+    if (use_direct_pair(L, x_dtype, y_dtype, compute))
+        return x_dtype == SEGB_U8_HWC ? launch_direct_pair_u8(a, L->w_pair.data(), st)
+                                      : launch_direct_pair_f32(a, L->w_pair.data(), st);
     if (x_dtype == SEGB_U8_HWC) return launch_direct_u8(a, ref, st);
     switch (compute) {
         case SEGB_F32:
@@ -471,6 +493,9 @@ int segb_describe_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h
     if (int rc = plan_forward(L, x_dtype, batch, in_h, in_w, y_dtype, compute, path, pl)) return rc;
     const char *name = "K2 direct (fp32 FFMA)";
     if (pl.path == SEGB_PATH_IGEMM) name = igemm_kernel_name(pl.s);
+    else if (use_direct_pair(L, x_dtype, y_dtype, pl.compute))
+        name = x_dtype == SEGB_U8_HWC ? "K2p direct (u8 image decoded on load, fp32 FFMA2, two samples per thread)"
+                                      : "K2p direct (fp32 FFMA2, two samples per thread)";
     else if (x_dtype == SEGB_U8_HWC) name = "K2 direct (u8 image decoded on load, fp32 FFMA)";
     else if (pl.compute == SEGB_F64) name = "K2 direct (fp64)";
     else if (pl.compute == SEGB_BF16) name = "K2 direct (bf16 operands, fp32 FFMA)";

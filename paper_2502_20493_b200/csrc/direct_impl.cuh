@@ -436,4 +436,16 @@ int launch_direct_bf16(const DirectArgs &a, int x_dtype, int y_dtype, bool ref_e
 // fp32 compute on the interleaved u8 image payload (x: (B, H, W, C), decoded on load)
 int launch_direct_u8(const DirectArgs &a, bool ref_engine, cudaStream_t st);
 
+// K2p, the paired FFMA2 kernel for low-channel layers (direct_pair.cuh): whether it takes a
+// segregated fp32 layer, and its launchers (x f32 / u8 image; w_host = the K2 weights
+// [c_out][c_in][n2p] on the host, passed as a kernel parameter)
+constexpr int kPairWMax = 896;
+inline bool direct_pair_ok(int c_in, int c_out, int n, int n2p) {
+    // n <= 3: K2's one-sample 8 x 4 tiles load fewer window values per output and win (ds224_k3
+    // 0.025 vs 0.028 ms); n 4, 5: K2p (ds512_k5 0.150 -> 0.129 ms, ds512_k4_c3 0.351 -> 0.298)
+    return c_out >= 1 && c_out <= 3 && n >= 4 && n <= 5 && (int64_t)c_in * c_out * n2p <= kPairWMax;
+}
+int launch_direct_pair_f32(const DirectArgs &a, const float *w_host, cudaStream_t st);
+int launch_direct_pair_u8(const DirectArgs &a, const float *w_host, cudaStream_t st);
+
 }  // namespace segb

@@ -1,0 +1,196 @@
+// K2p -- the direct kernel for the low-channel layers (dataset images; n = 4, 5, c_out <= 3 and a
+// weight tensor of at most kPairWMax floats), fp32 compute with packed FFMA2.
+//
+// Same per-element rule, summation order and outputs as K2 (direct_impl.cuh; spec
+// /root/reference/pkg/src/segconv/engines.py:379-406, ascending ci as engines.py:163-172), so
+// the results are bitwise K2's. What differs is the mapping onto the SM:
+//   - two samples per thread: every register of the input window and of the accumulators is a
+//     float2 (sample b in .x, sample b + 1 in .y), so each multiply-add of the rule is one lane of
+//     an FFMA2 (sm_100: two fp32 FMAs per instruction) -- half the FMA instructions of K2, and
+//     the pairs come straight from the loads (no register shuffling);
+//   - the class-packed weights are a __grid_constant__ kernel parameter: warp-uniform values the
+//     FFMA2s read as uniform-register broadcast operands, so they take no vector registers and no
+//     shared-memory traffic (K2 stages them through shared memory and holds a tap vector in
+//     registers, which spilled for n = 5 under the six-blocks-per-SM register cap).
+#pragma once
+
+#include "direct_impl.cuh"
+
+namespace segb {
+
+struct PairWeights {  // kPairWMax (direct_impl.cuh) floats: a 3.5 KB kernel parameter
+    float w[kPairWMax];
+};
+
+template <typename TX, int N, int COB, int RQ, int CQ>
+// (one channel: 2 x 2 quads, 64 live float registers of window and accumulators -> 5 blocks per
+// SM so nothing spills; two: 2 x 1 quads in 80 registers, 6 blocks; three: 4 blocks)
+__global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
+    direct_pair_kernel(DirectArgs a, const __grid_constant__ PairWeights W) {
+    constexpr int NW = N / 2 + 1;    // input rows/cols under one output quad
+    constexpr int WR = RQ + NW - 1;  // window rows for RQ row quads
+    constexpr int WC = CQ + NW - 1;  // window cols for CQ column quads
+    constexpr int R0 = (N + 1) / 2, R1 = N / 2;
+    constexpr int OFF1 = R0 * R0, OFF2 = R0 * R0 + R0 * R1, OFF3 = R0 * R0 + 2 * R0 * R1;
+    constexpr int N2P = (N * N + 3) / 4 * 4;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const int t0 = (blockIdx.x * 32 + threadIdx.x) * CQ;  // first column quad
+    const int q0 = (blockIdx.y * kDirectRowsPerBlock + threadIdx.y) * RQ;
+    const int64_t b = a.b0 + 2 * (int64_t)blockIdx.z;  // samples b and b + 1 (if it exists)
+    const bool two = b + 1 < a.batch;
+    const int row0 = q0 - a.swap - a.p, col0 = t0 - a.swap - a.p;
+    const int64_t plane = (int64_t)a.h * a.w_in;
+    constexpr bool HWC = XLayout<TX>::HWC;
+    const int es = HWC ? a.c_in : 1;              // column (element) stride
+    const int64_t rs = (int64_t)a.w_in * es;      // row stride
+    const int64_t cs = XLayout<TX>::chan(plane);  // channel stride
+    const int64_t ss = (int64_t)a.c_in * plane;   // sample stride
+    const TX *xb = reinterpret_cast<const TX *>(a.x) + b * ss;
+
+    float2 acc[COB][2 * RQ][2 * CQ];
+#pragma unroll
+    for (int c = 0; c < COB; ++c)
+#pragma unroll
+        for (int i = 0; i < 2 * RQ; ++i)
+#pragma unroll
+            for (int k = 0; k < 2 * CQ; ++k) acc[c][i][k] = make_float2(0.f, 0.f);
+
+    const bool inside = row0 >= 0 && row0 + WR <= a.h && col0 >= 0 && col0 + WC <= a.w_in;
+    const bool warp_inside = __all_sync(0xffffffffu, inside) && __all_sync(0xffffffffu, two);
+    bool rok[WR], cok[WC];
+#pragma unroll
+    for (int i = 0; i < WR; ++i) rok[i] = (unsigned)(row0 + i) < (unsigned)a.h;
+#pragma unroll
+    for (int j = 0; j < WC; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
+    const TX *xw = xb + (int64_t)row0 * rs + (int64_t)col0 * es;  // window origin (may point outside)
+
+    float2 win[WR][WC];
+#pragma unroll 1
+    for (int ci = 0; ci < a.c_in; ++ci) {
+        const TX *xc = xw + (int64_t)ci * cs;
+        if (warp_inside) {
+#pragma unroll
+            for (int i = 0; i < WR; ++i)
+#pragma unroll
+                for (int j = 0; j < WC; ++j) {
+                    const TX *p = xc + i * rs + j * es;
+                    win[i][j] = make_float2(load_x<TX, float, false>(p), load_x<TX, float, false>(p + ss));
+                }
+        } else {
+#pragma unroll
+            for (int i = 0; i < WR; ++i)
+#pragma unroll
+                for (int j = 0; j < WC; ++j) {
+                    const TX *p = xc + i * rs + j * es;
+                    const bool ok = rok[i] && cok[j];
+                    win[i][j] = make_float2(ok ? load_x<TX, float, false>(p) : 0.f,
+                                            (ok && two) ? load_x<TX, float, false>(p + ss) : 0.f);
+                }
+        }
+#pragma unroll
+        for (int c = 0; c < COB; ++c) {
+            const float *wv = W.w + (c * a.c_in + ci) * N2P;  // uniform: broadcast operands
+            auto fma2 = [&](float2 &d, const float2 &x, float w) { d = __ffma2_rn(x, make_float2(w, w), d); };
+#pragma unroll
+            for (int qq = 0; qq < RQ; ++qq)
+#pragma unroll
+                for (int cq = 0; cq < CQ; ++cq) {
+#pragma unroll
+                    for (int u = 0; u < R0; ++u) {
+#pragma unroll
+                        for (int v = 0; v < R0; ++v) fma2(acc[c][2 * qq][2 * cq], win[qq + u][cq + v], wv[u * R0 + v]);
+#pragma unroll
+                        for (int v = 0; v < R1; ++v)
+                            fma2(acc[c][2 * qq][2 * cq + 1], win[qq + u][cq + 1 + v], wv[OFF1 + u * R1 + v]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < R1; ++u) {
+#pragma unroll
+                        for (int v = 0; v < R0; ++v)
+                            fma2(acc[c][2 * qq + 1][2 * cq], win[qq + 1 + u][cq + v], wv[OFF2 + u * R0 + v]);
+#pragma unroll
+                        for (int v = 0; v < R1; ++v)
+                            fma2(acc[c][2 * qq + 1][2 * cq + 1], win[qq + 1 + u][cq + 1 + v], wv[OFF3 + u * R1 + v]);
+                    }
+                }
+        }
+    }
+
+    // stores as K2: staged per warp through shared memory so each store instruction writes 32
+    // consecutive outputs of one row; one sample at a time
+    constexpr int SC = 64 * CQ;
+    float *stg = reinterpret_cast<float *>(smem_raw) + threadIdx.y * (COB * 2 * RQ * SC);
+    float *yb = reinterpret_cast<float *>(a.y);
+    const int y0 = 2 * (blockIdx.x * 32 * CQ) - a.swap;  // first output column of the warp
+#pragma unroll
+    for (int sidx = 0; sidx < 2; ++sidx) {
+        if (sidx == 1 && !two) break;
+#pragma unroll
+        for (int c = 0; c < COB; ++c)
+#pragma unroll
+            for (int i = 0; i < 2 * RQ; ++i)
+#pragma unroll
+                for (int k = 0; k < 2 * CQ; ++k)
+                    stg[(c * 2 * RQ + i) * SC + threadIdx.x * 2 * CQ + k] = sidx ? acc[c][i][k].y : acc[c][i][k].x;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < COB; ++c) {
+            float *yc = yb + ((b + sidx) * a.c_out + c) * a.oh * a.ow;
+#pragma unroll
+            for (int i = 0; i < 2 * RQ; ++i) {
+                const int xo = 2 * q0 + i - a.swap;
+                if ((unsigned)xo >= (unsigned)a.oh) continue;
+                float *row = yc + (int64_t)xo * a.ow;
+#pragma unroll
+                for (int m = 0; m < 2 * CQ; ++m) {
+                    const int col = m * 32 + threadIdx.x;
+                    const int yo = y0 + col;
+                    if ((unsigned)yo < (unsigned)a.ow) row[yo] = stg[(c * 2 * RQ + i) * SC + col];
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <typename TX, int N, int COB>
+int launch_direct_pair_n(const DirectArgs &a, const PairWeights &W, cudaStream_t st) {
+    // one channel: 2 x 2 quads (window 4 x 4 pairs); two or three channels: 2 x 1
+    constexpr int RQ = 2, CQ = COB == 1 ? 2 : 1;
+    dim3 block(32, kDirectRowsPerBlock);
+    const int64_t nrb = ceil_div(a.nqr, kDirectRowsPerBlock * RQ);
+    if (nrb > 65535) return fail(SEGB_ERR_UNSUPPORTED, "output too large for the paired direct kernel grid");
+    const size_t smem = sizeof(float) * kDirectRowsPerBlock * COB * 2 * RQ * 64 * CQ;
+    const int64_t pairs = ceil_div(a.batch, 2);
+    for (int64_t p0 = 0; p0 < pairs; p0 += 65535) {
+        DirectArgs c = a;
+        c.b0 = 2 * p0;
+        dim3 grid((unsigned)ceil_div(a.nqc, 32 * CQ), (unsigned)nrb, (unsigned)std::min<int64_t>(65535, pairs - p0));
+        direct_pair_kernel<TX, N, COB, RQ, CQ><<<grid, block, smem, st>>>(c, W);
+        note_launch();
+        if (int rc = check_launch("direct_pair_kernel")) return rc;
+    }
+    return SEGB_OK;
+}
+
+template <typename TX, int N>
+int launch_direct_pair_cob(const DirectArgs &a, const PairWeights &W, cudaStream_t st) {
+    if (a.c_out == 1) return launch_direct_pair_n<TX, N, 1>(a, W, st);
+    if (a.c_out == 2) return launch_direct_pair_n<TX, N, 2>(a, W, st);
+    return launch_direct_pair_n<TX, N, 3>(a, W, st);
+}
+
+// w_host: the K2 class-packed weights [c_out][c_in][n2p] (fp32) on the host
+template <typename TX>
+int launch_direct_pair(const DirectArgs &a, const float *w_host, cudaStream_t st) {
+    PairWeights W;
+    const int64_t nw = (int64_t)a.c_in * a.c_out * a.n2p;
+    if (!direct_pair_ok(a.c_in, a.c_out, a.n, a.n2p) || !w_host)
+        return fail(SEGB_ERR_UNSUPPORTED, "paired direct kernel: unsupported layer");
+    for (int64_t i = 0; i < nw; ++i) W.w[i] = w_host[i];
+    if (a.n == 4) return launch_direct_pair_cob<TX, 4>(a, W, st);
+    return launch_direct_pair_cob<TX, 5>(a, W, st);
+}
+
+}  // namespace segb
