@@ -544,18 +544,32 @@ __global__ void nchw_to_nhwc_bf16(const TX *__restrict__ x, __nv_bfloat16 *__res
     }
 }
 
-// Vectorised path (HW % 8 == 0, C % 8 == 0): thread (cg = t & 7, hc = t >> 3) of a
-// 256-thread block loads an 8-channel x 8-position tile with 128-bit loads, transposes
-// it in registers with byte permutes and writes 8 x 128-bit channels-last rows.
-// Block tile: 64 channels x 256 positions; no shared memory.
+// The 8-channel x 8-position tile of staging thread i (flat grid of nthreads = B x HW/8 x
+// ceil(C/64) x 8): lane bits 0-2 pick the channel group of a 64-channel block (writes: 8 x 16 B
+// contiguous), then position chunks, then channel blocks and samples -- every thread has work
+// for any HW (a 256-position x 64-channel block per CTA left 15 of 16 threads idle at HW = 16).
+__device__ __forceinline__ bool staging_tile(int C, int HW, int64_t nthreads, int64_t &b, int &c0, int &hw0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nthreads) return false;
+    const int nhc = HW / 8, ncb = (C + 63) / 64;
+    const int64_t r = i >> 3;
+    const int hc = (int)(r % nhc);
+    const int64_t r2 = r / nhc;
+    c0 = (int)(r2 % ncb) * 64 + (int)(i & 7) * 8;
+    b = r2 / ncb;
+    hw0 = hc * 8;
+    return c0 < C;
+}
+
+// Vectorised path (HW % 8 == 0, C % 8 == 0): each thread (staging_tile) loads an 8-channel x
+// 8-position tile with 128-bit loads, transposes it in registers with byte permutes and writes
+// 8 x 128-bit channels-last rows; no shared memory.
 template <typename TX>
 __global__ void __launch_bounds__(256) nchw_to_nhwc_bf16_v8(const TX *__restrict__ x, __nv_bfloat16 *__restrict__ y,
-                                                             int C, int HW) {
-    const int64_t b = blockIdx.z;
-    const int cg = threadIdx.x & 7, hc = threadIdx.x >> 3;
-    const int c0 = blockIdx.y * 64 + cg * 8;
-    const int hw0 = blockIdx.x * 256 + hc * 8;
-    if (c0 >= C || hw0 >= HW) return;
+                                                             int C, int HW, int64_t nthreads) {
+    int64_t b;
+    int c0, hw0;
+    if (!staging_tile(C, HW, nthreads, b, c0, hw0)) return;
     const TX *src = x + (b * C + c0) * (int64_t)HW + hw0;
     uint32_t r[8][4];  // r[c][k]: channel c, positions 2k, 2k+1 (bf16 pairs)
 #pragma unroll
@@ -620,11 +634,11 @@ __global__ void nchw_to_nhwc_tf32x2(const float *__restrict__ x, float *__restri
 }
 
 // NCHW fp32 -> NHWC fp16 hi / lo planes of the 3xFP16 A operand, scaled by 2^k_x (k_x from the
-// input's absmax partials, f16split.cuh). Thread (cg = t & 7, hc = t >> 3) of a 256-thread block
-// loads an 8-channel x 8-position tile with 128-bit loads, splits it and transposes the fp16 pairs
+// input's absmax partials, f16split.cuh). Each thread (staging_tile) loads an 8-channel x
+// 8-position tile with 128-bit loads, splits it and transposes the fp16 pairs
 // in registers (byte permutes) into 8 channels-last 16-byte rows per plane. HW % 8 == 0, C % 8 == 0.
 __global__ void __launch_bounds__(256) nchw_to_nhwc_f16x2_v8(const float *__restrict__ x, __half *__restrict__ hi,
-                                                              __half *__restrict__ lo, int C, int HW,
+                                                              __half *__restrict__ lo, int C, int HW, int64_t nthreads,
                                                               const float *__restrict__ partials) {
     __shared__ float scale;
     if (threadIdx.x < 32) {
@@ -635,11 +649,9 @@ __global__ void __launch_bounds__(256) nchw_to_nhwc_f16x2_v8(const float *__rest
     }
     __syncthreads();
     const float sc = scale;
-    const int64_t b = blockIdx.z;
-    const int cg = threadIdx.x & 7, hc = threadIdx.x >> 3;
-    const int c0 = blockIdx.y * 64 + cg * 8;
-    const int hw0 = blockIdx.x * 256 + hc * 8;
-    if (c0 >= C || hw0 >= HW) return;
+    int64_t b;
+    int c0, hw0;
+    if (!staging_tile(C, HW, nthreads, b, c0, hw0)) return;
     const float *src = x + (b * C + c0) * (int64_t)HW + hw0;
     uint32_t rh[8][4], rl[8][4];  // [channel][k]: positions 2k, 2k+1 as fp16 pairs
 #pragma unroll
@@ -955,9 +967,9 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
         if (mode == kModeF16x3) {
             if (int rc = run_absmax_partials(x, SEGB_F32, elems, partials, st)) return rc;
             if (hw % 8 == 0 && s.c_in % 8 == 0) {
-                dim3 grd((unsigned)ceil_div(hw, 256), (unsigned)ceil_div(s.c_in, 64), (unsigned)s.batch);
-                nchw_to_nhwc_f16x2_v8<<<grd, 256, 0, st>>>((const float *)x, (__half *)xs, (__half *)xs_lo, s.c_in, hw,
-                                                           partials);
+                const int64_t nth = s.batch * (hw / 8) * ceil_div(s.c_in, 64) * 8;
+                nchw_to_nhwc_f16x2_v8<<<(unsigned)ceil_div(nth, 256), 256, 0, st>>>(
+                    (const float *)x, (__half *)xs, (__half *)xs_lo, s.c_in, hw, nth, partials);
             } else {
                 const unsigned g = (unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 64);
                 nchw_to_nhwc_f16x2<<<g, 256, 0, st>>>((const float *)x, (__half *)xs, (__half *)xs_lo, s.c_in, hw, elems,
@@ -967,12 +979,14 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
             const unsigned g = (unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 64);
             nchw_to_nhwc_tf32x2<<<g, 256, 0, st>>>((const float *)x, (float *)xs, (float *)xs_lo, s.c_in, hw, elems);
         } else if (hw % 8 == 0 && s.c_in % 8 == 0) {
-            dim3 grd((unsigned)ceil_div(hw, 256), (unsigned)ceil_div(s.c_in, 64), (unsigned)s.batch);
+            const int64_t nth = s.batch * (hw / 8) * ceil_div(s.c_in, 64) * 8;
+            const unsigned grd = (unsigned)ceil_div(nth, 256);
             if (s.x_dtype == SEGB_BF16)
                 nchw_to_nhwc_bf16_v8<__nv_bfloat16><<<grd, 256, 0, st>>>((const __nv_bfloat16 *)x,
-                                                                         (__nv_bfloat16 *)xs, s.c_in, hw);
+                                                                         (__nv_bfloat16 *)xs, s.c_in, hw, nth);
             else
-                nchw_to_nhwc_bf16_v8<float><<<grd, 256, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw);
+                nchw_to_nhwc_bf16_v8<float><<<grd, 256, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw,
+                                                                 nth);
         } else {
             dim3 blk(32, 8), grd((unsigned)ceil_div(hw, 32), (unsigned)ceil_div(s.c_in, 32), (unsigned)s.batch);
             if (s.x_dtype == SEGB_BF16)
