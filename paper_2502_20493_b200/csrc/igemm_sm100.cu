@@ -52,6 +52,9 @@ constexpr int kTf32Chunk = 8;
 #define SEGB_F16X3_CHUNK 4
 #endif
 constexpr int kF16Chunk = SEGB_F16X3_CHUNK;
+#ifndef SEGB_K3_NACC3
+#define SEGB_K3_NACC3 4
+#endif
 constexpr int kTf32MaxN = 128;
 
 // instruction descriptor: fp16 x fp16 -> fp32, A and B K-major, M = 128, N = n
@@ -112,6 +115,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int KCH = kstep_channels<MODE>();
     constexpr int NOP = TF32X3 ? 2 : 1;  // tiles per operand per stage (hi [, lo])
     constexpr int CHUNK = MODE == kModeF16x3 ? kF16Chunk : kTf32Chunk;  // k-steps per TMEM partial
+    // TMEM accumulator buffers: the 3-pass modes (N <= 128) keep four, so the MMAs run up to three
+    // partials ahead while the epilogue writes a finished tile (with two, a tile's output stores
+    // held the next tile's second partial; fp32 ebgan_l5 has only four partials per tile)
+    constexpr int NACC = TF32X3 ? SEGB_K3_NACC3 : 2;
     // PM 3 (SWAP): a single CTA with the operands swapped -- A = 128 output channels of weights,
     // B = the tile's class positions (N = 16..128): tiny batches, where a 128-position A box would be
     // mostly zero fill and the weights are the bytes that matter
@@ -128,8 +135,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *full = reinterpret_cast<uint64_t *>(sB + S * NOP * b_cta);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
-    uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *tempty = tfull + NACC;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NACC);
     float *unscale_slot = reinterpret_cast<float *>(tmem_slot + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], PM == 1 ? 2 : 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NACC; ++i) {
             mbar_init(&tfull[i], 1);
             // TWO: the leader's counts its 4 epilogue warps + 1 forwarded arrival from the peer
             mbar_init(&tempty[i], TWO && rank == 0 ? 5 : 4);
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) *unscale_slot = ldexpf(1.f, -f16_scale_exp(m)) * prm.w_unscale;
     }
     if (warp == 1) {  // TMEM: two accumulator buffers of N fp32 columns
-        const uint32_t cols = tmem_cols(N);
+        const uint32_t cols = NACC == 2 ? tmem_cols(N) : tmem_pow2(NACC * N);
         if (TWO) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                              smem_u32(tmem_slot)),
@@ -305,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (kc == 0) {
                         if (ks > 0) {
                             commit(&tfull[acc], false);
-                            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                            if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
                         }
                         mbar_wait(&tempty[acc], acc_phase ^ 1);
                         tc_fence_after();
@@ -331,12 +338,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++stage == S_) { stage = 0; phase ^= 1; }
                 }
                 commit(&tfull[acc], false);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
             }
         } else if (lane == 0) {  // ---------------- TWO, peer: forward "TMEM buffer drained" to the leader
             int acc = 0;
             uint32_t acc_phase = 0;
-            const uint32_t lt[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
+            uint32_t lt[NACC];
+#pragma unroll
+            for (int i = 0; i < NACC; ++i) lt[i] = mapa_rank(&tempty[i], 0);
             for (int t = t_begin; t < prm.total_tiles; t += t_step) {
                 int k_lo, k_hi;
                 krange(t, k_lo, k_hi);
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < uses; ++k) {
                     mbar_wait(&tempty[acc], acc_phase);
                     mbar_arrive_cluster(lt[acc]);
-                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                    if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
                 }
             }
         }
@@ -381,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(acc);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
             }
             if (co < prm.c_out) {
                 const int64_t per = (int64_t)g.rows * g.cols;
@@ -436,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) release_acc(acc);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
             }
             const int64_t pos = (int64_t)mb * kBlockM + m;
             if (pos < prm.class_positions && prm.ksplit > 1) {  // split K: this range's fp32 partial
@@ -506,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) release_acc(acc);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (TWO) cluster_sync_all();  // the leader's MMAs write this CTA's TMEM until both are done
     if (warp == 1) {
         tc_fence_after();
-        const uint32_t cols = tmem_cols(N);
+        const uint32_t cols = NACC == 2 ? tmem_cols(N) : tmem_pow2(NACC * N);
         if (TWO) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
         else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols));
     }
@@ -1050,7 +1059,7 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t b_cta = (size_t)(pm == 2 ? prm.n_tile / 2 : prm.n_tile) * 128;
     const size_t stage_bytes = (size_t)(tf32 ? 2 : 1) * ((size_t)kBlockM * 128 + b_cta);
-    const size_t smem = 1024 + prm.stages * stage_bytes + (2 * prm.stages + 4) * 8 + 16;
+    const size_t smem = 1024 + prm.stages * stage_bytes + (2 * prm.stages + 8) * 8 + 16;  // up to 4 TMEM buffers
     const unsigned grid = pair ? 2 * (unsigned)std::min<int64_t>(prm.total_tiles, sms / 2)
                                : (unsigned)std::min<int64_t>(prm.total_tiles, sms);
 #define SEGB_K3_LAUNCH(TY_, TF_)                                                                       \
