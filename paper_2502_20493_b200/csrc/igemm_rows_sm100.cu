@@ -52,6 +52,12 @@ constexpr int kLoaderWarp0 = 8;                               // first of the 4 
 constexpr int kRowsThreads = 12 * 32;                         // launch budget: 168 registers
 constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168 + 232) <= 64 K
 // 3xFP16: the epilogue holds a whole tile's accumulators (4 classes x 32 columns) at once
+#ifndef SEGB_ROWS_BF16_STCS  // the same for the bf16 epilogue
+#define SEGB_ROWS_BF16_STCS 1  // measured: ebgan_l7 bf16 0.577 -> 0.567 ms
+#endif
+#ifndef SEGB_ROWS_F16_STCS
+#define SEGB_ROWS_F16_STCS 1  // measured: ebgan_l7 fp32 1.728 -> 1.681 ms, l6 0.976 -> 0.964
+#endif
 #ifndef SEGB_ROWS_F16_ST16  // 3xFP16 epilogue stores: 16-byte (lane-pair exchange) or two 8-byte per channel
 #define SEGB_ROWS_F16_ST16 0  // measured: 8-byte stores without exchange -3.5% (l7), -8% (l6) vs 16-byte
 #endif
@@ -1119,8 +1125,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                                     a0 = make_float2(old[k].x + r0.x, old[k].y + r0.y);
                                     a1 = make_float2(old[k].z + r1.x, old[k].w + r1.y);
                                 }
+#if SEGB_ROWS_F16_STCS  // streaming (evict-first) stores: the output does not push the input rows out of L2
+                                __stcs(d0, a0);
+                                __stcs(reinterpret_cast<float2 *>(pf + (int64_t)co * plane + prm.ow), a1);
+#else
                                 d0[0] = a0;
                                 *reinterpret_cast<float2 *>(pf + (int64_t)co * plane + prm.ow) = a1;
+#endif
                             }
 #endif
                         }
@@ -1260,7 +1271,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     for (int rr = 0; rr < (RS != 2 && !HALF ? 2 : 1); ++rr) {
                         const uint32_t got = __shfl_xor_sync(0xffffffffu, sent[rr], 1);
                         const uint2 v = odd ? make_uint2(got, mine[rr]) : make_uint2(mine[rr], got);
-                        if (lane_active && !(ABL(1))) *reinterpret_cast<uint2 *>(pc2 + rr * ow_b) = v;
+                        if (lane_active && !(ABL(1))) {
+                            if (SEGB_ROWS_BF16_STCS) __stcs(reinterpret_cast<uint2 *>(pc2 + rr * ow_b), v);
+                            else *reinterpret_cast<uint2 *>(pc2 + rr * ow_b) = v;
+                        }
                     }
                     pc2 += 2 * plane_b;
                 }
