@@ -87,6 +87,9 @@ def load_peaks():
         with open(path) as f:
             d = json.load(f)
         out.update(hbm_gbs=d["hbm_gbs"], bf16_tflops=d["bf16_tflops"], source="measured (MEASURED_PEAKS.json)")
+        # long steps run power-capped (sw_power_cap): the driver's sustained / burst bf16 ratio
+        # scales the compute roofs of kernels timed inside the step ("frac_sustained")
+        out["sustained_ratio"] = d.get("bf16_tflops_sustained", d["bf16_tflops"]) / d["bf16_tflops"]
     with open(os.path.join(ROOT, "profiles", "r2_peaks.json")) as f:
         p = json.load(f)
     # the FP32 FMA roof of the direct kernel: register-operand FFMA2 (packed, two FMAs per lane), the
@@ -601,6 +604,8 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
         layer_rows.append({"name": s["name"], "path": s["path"], "kernel": s["kernel"], "ms": lms,
                            "gmacs": s["macs"] / (lms * 1e-3) / 1e9, "bound": bound, "peak_name": cname,
                            "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                           "frac_sustained": achieved / (peak * peaks.get("sustained_ratio", 1.0)) if bound != "hbm"
+                           else achieved / peak,
                            "alg_bytes": s["bytes"], "flops": s["flops"]})
     dom = max(layer_rows, key=lambda r: r["ms"])
     traffic = None
@@ -692,7 +697,7 @@ def run_ours(args, rank, world, local_rank):
         companion = {"workload": COMPANION[wl], "dtype": "bf16", "value": c["value"], "unit": "GMAC/s",
                      "ms_per_step": c["ms_per_step"], "roofline": c["roofline"], "parity": c["parity"],
                      "e2e": c["e2e"], "gpu_launches": c["gpu_launches"], "clocks": c["clocks"],
-                     "layers": [{k: row[k] for k in ("name", "kernel", "ms", "gmacs", "bound", "frac")}
+                     "layers": [{k: row[k] for k in ("name", "kernel", "ms", "gmacs", "bound", "frac", "frac_sustained")}
                                 for row in c["layers"]]}
     if rank != 0:
         return 0
