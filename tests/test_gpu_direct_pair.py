@@ -70,3 +70,19 @@ def test_pair_not_taken_outside_its_range(torch):
         assert not layer.describe_path(2, 16, 16).startswith("K2p")
     layer = P.prepare_layer(O.gen_kernel_bank(3, 1, 5, 1), 2, engine="reference")
     assert not layer.describe_path(2, 16, 16).startswith("K2p")
+
+
+@pytest.mark.parametrize("batch,c_in,c_out,n,pad,h,w", [(3, 3, 1, 5, 2, 37, 53), (5, 2, 3, 4, 1, 9, 70),
+                                                         (1, 3, 2, 4, 3, 1, 1)])
+def test_pair_writes_exactly_the_output(torch, batch, c_in, c_out, n, pad, h, w):
+    """every output element written once, nothing around it: y is a window of a NaN-filled buffer"""
+    layer = P.prepare_layer(O.gen_kernel_bank(c_in, c_out, n, 2), pad)
+    oh, ow = layer.output_shape(h, w)
+    count, guard = batch * c_out * oh * ow, 4096
+    buf = torch.full((count + 2 * guard,), float("nan"), device="cuda")
+    y = buf[guard:guard + count].view(batch, c_out, oh, ow)
+    x = torch.rand((batch, c_in, h, w), device="cuda")
+    layer.forward(x, out=y)
+    torch.cuda.synchronize()
+    assert not torch.isnan(y).any()
+    assert torch.isnan(buf[:guard]).all() and torch.isnan(buf[guard + count:]).all()
