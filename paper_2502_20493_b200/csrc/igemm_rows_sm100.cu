@@ -680,12 +680,42 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     c.l = nr - 1;  // consecutive tiles of a strip share nr - 1 rows
                 }
             };
+#ifndef SEGB_ROWS_F16_LOADS_V2
+#define SEGB_ROWS_F16_LOADS_V2 1
+#endif
+            // c_in % 8 == 0 (rows_params): a thread's 8 channels are all valid or all past c_in, so
+            // one predicate per unit and a running pointer per channel (the per-channel 64-bit
+            // address arithmetic, predicates and zero-fills spilled the base pointer back to the
+            // constant bank and stalled on address-register reuse behind queued loads)
+            const int64_t plane4 = plane_in / 4;  // plane_in % 4 == 0 (prm.w % 8 == 0)
             auto load_unit = [&](const Cur &u, float4 (&r)[8], float (&hv)[8]) {
                 const int row = u.i + dminr + u.l;
                 const int j0 = u.ms * MR;
                 const bool in_row = row >= 0 && row < prm.h;
                 const int ch0 = prm.ch_base + cg * 8;
                 const float *src = xf + ((int64_t)u.b * prm.c_in + ch0) * plane_in + (int64_t)row * prm.w + j0;
+#if SEGB_ROWS_F16_LOADS_V2
+                const bool ok = in_row && ch0 < prm.c_in && !(ABL(2));
+                if (ok) {
+                    const float4 *q = reinterpret_cast<const float4 *>(src) + c4;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) r[c] = __ldg(q + c * plane4);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) r[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) hv[c] = 0.f;
+                if (th < (HL + HR) * 8) {  // halo column tasks: (halo col, channel group)
+                    const int hc = th >> 3;
+                    const int col = hc < HL ? j0 - HL + hc : j0 + MR + (hc - HL);
+                    if (ok && col >= 0 && col < prm.w) {
+                        const float *q = src + (col - j0);
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) hv[c] = __ldg(q + c * plane_in);
+                    }
+                }
+#else
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     r[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -703,6 +733,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                             if (ch0 + c < prm.c_in) hv[c] = __ldg(src + (int64_t)c * plane_in + (col - j0));
                     }
                 }
+#endif
             };
             static_assert(KBC == 1 && !PAIRKB, "3xFP16 rows: one 64-channel block per pass");
             float4 rb[KLB][8];
