@@ -590,6 +590,7 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
     total_macs = sum(layer_stats(c, batch if scaling == "strong" else batch * world, dtype)[0] for c in layers)
     value = total_macs / (ms * 1e-3) / 1e9
 
+    capped = bool(clocks) and "sw_power_cap" in (clocks.get("reasons") or [])
     layer_rows = []
     for j, s in enumerate(state):
         lms = float(np.mean(per_layer[j]))
@@ -604,8 +605,9 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
         layer_rows.append({"name": s["name"], "path": s["path"], "kernel": s["kernel"], "ms": lms,
                            "gmacs": s["macs"] / (lms * 1e-3) / 1e9, "bound": bound, "peak_name": cname,
                            "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                           "frac_sustained": achieved / (peak * peaks.get("sustained_ratio", 1.0)) if bound != "hbm"
-                           else achieved / peak,
+                           # against the driver's sustained peak, for runs that hit the power cap
+                           "frac_sustained": (achieved / (peak * peaks.get("sustained_ratio", 1.0)) if bound != "hbm"
+                                              else achieved / peak) if capped else None,
                            "alg_bytes": s["bytes"], "flops": s["flops"]})
     dom = max(layer_rows, key=lambda r: r["ms"])
     traffic = None

@@ -344,6 +344,12 @@ bool cp_params(const IgemmShape &s, CpParams &prm) {
     prm.m_pairs = (prm.m_tiles + 1) / 2;
     const int64_t total = 2ll * prm.m_pairs * prm.n_blocks;
     if (total > INT32_MAX) return false;
+    // too few pair tiles to fill half the SM pairs (small batches): K3 with narrow N tiles and
+    // split K spreads the layer wider (dcgan_l4 bf16 at batch 1: 24.6 -> 18.4 us; batch 16: 24.6
+    // -> 22.5). SEGB200_K3P_MIN_TILES overrides (tests run K3p at small shapes with 0).
+    int64_t min_tiles = 37;
+    if (const char *mt = getenv("SEGB200_K3P_MIN_TILES")) min_tiles = atoll(mt);
+    if (total < min_tiles) return false;
     prm.total_tiles = (int)total;
     const int stage_bytes = kBlockM * 128 + nb_w * 128;
     prm.stages = std::min(kCpMaxStages, (int)((227 * 1024 - 1024 - 256) / stage_bytes));

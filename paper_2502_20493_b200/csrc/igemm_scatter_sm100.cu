@@ -280,6 +280,12 @@ bool scatter_params(const IgemmShape &s, ScatterParams &prm) {
     prm.positions = s.batch * hw;
     const int64_t tiles = ceil_div(prm.positions, 128);
     if (tiles > INT32_MAX) return false;
+    // small batches (few 128-position tiles): the output-stationary K3 with split K is faster
+    // (dcgan_l5 bf16 at batch 1: 18.4 -> 16.4 us; at batch 16 K3c wins, 18.9 vs 22.5).
+    // SEGB200_K3C_MIN_TILES overrides (tests run K3c at small shapes with 0).
+    int64_t min_tiles = 64;
+    if (const char *mt = getenv("SEGB200_K3C_MIN_TILES")) min_tiles = atoll(mt);
+    if (tiles < min_tiles) return false;
     prm.hw = (int)hw;
     prm.c_in = s.c_in;
     prm.n_real = nreal;

@@ -553,6 +553,14 @@ __global__ void nchw_to_nhwc_bf16(const TX *__restrict__ x, __nv_bfloat16 *__res
     }
 }
 
+// threads per staging block: 256, fewer for small inputs (batch 1: DCGAN l2 stages 256 tiles,
+// which as one 256-thread block ran on a single SM)
+inline int staging_block(int64_t nthreads) {
+    int tpb = 256;
+    while (tpb > 32 && ceil_div(nthreads, tpb) < 2 * 148) tpb /= 2;
+    return tpb;
+}
+
 // The 8-channel x 8-position tile of staging thread i (flat grid of nthreads = B x HW/8 x
 // ceil(C/64) x 8): lane bits 0-2 pick the channel group of a 64-channel block (writes: 8 x 16 B
 // contiguous), then position chunks, then channel blocks and samples -- every thread has work
@@ -851,8 +859,14 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     prm.ksplit = 1;
     {
         const int nks = prm.cls[0].R * prm.cls[0].C * prm.k_cblocks;
-        if (total < 74 && nks >= 8)
-            prm.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>({8, nks / 4, ceil_div(148, total)}));
+        // the largest split that still fits one wave (2-SM pairs, the default from two position
+        // tiles on: 74 slots of pair tiles; else 148): one more tile per slot would double the
+        // critical path (DCGAN l2 at batch 1: split 3 = 192 tiles on 148 SMs 21 us, split 2 ...)
+        const bool pairs = prm.m_tiles >= 2 && !prm.swap_ab;
+        const int64_t units = pairs ? 4ll * ((prm.m_tiles + 1) / 2) * prm.n_blocks : total;
+        const int64_t slots = pairs ? 74 : 148;
+        if (2 * units <= slots && nks >= 8)
+            prm.ksplit = (int)std::max<int64_t>(1, std::min<int64_t>({8, nks / 4, slots / units}));
         if (const char *e = getenv("SEGB200_K3_KSPLIT")) {  // A/B experiments
             const int v = atoi(e);
             if (v >= 1 && v <= 16 && v <= nks) prm.ksplit = v;
@@ -977,7 +991,8 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
             if (int rc = run_absmax_partials(x, SEGB_F32, elems, partials, st)) return rc;
             if (hw % 8 == 0 && s.c_in % 8 == 0) {
                 const int64_t nth = s.batch * (hw / 8) * ceil_div(s.c_in, 64) * 8;
-                nchw_to_nhwc_f16x2_v8<<<(unsigned)ceil_div(nth, 256), 256, 0, st>>>(
+                const int tpb = staging_block(nth);
+                nchw_to_nhwc_f16x2_v8<<<(unsigned)ceil_div(nth, tpb), tpb, 0, st>>>(
                     (const float *)x, (__half *)xs, (__half *)xs_lo, s.c_in, hw, nth, partials);
             } else {
                 const unsigned g = (unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 64);
@@ -989,12 +1004,13 @@ int run_igemm(const IgemmShape &s, const void *x, const void *wg, const void *wg
             nchw_to_nhwc_tf32x2<<<g, 256, 0, st>>>((const float *)x, (float *)xs, (float *)xs_lo, s.c_in, hw, elems);
         } else if (hw % 8 == 0 && s.c_in % 8 == 0) {
             const int64_t nth = s.batch * (hw / 8) * ceil_div(s.c_in, 64) * 8;
-            const unsigned grd = (unsigned)ceil_div(nth, 256);
+            const int tpb = staging_block(nth);
+            const unsigned grd = (unsigned)ceil_div(nth, tpb);
             if (s.x_dtype == SEGB_BF16)
-                nchw_to_nhwc_bf16_v8<__nv_bfloat16><<<grd, 256, 0, st>>>((const __nv_bfloat16 *)x,
+                nchw_to_nhwc_bf16_v8<__nv_bfloat16><<<grd, tpb, 0, st>>>((const __nv_bfloat16 *)x,
                                                                          (__nv_bfloat16 *)xs, s.c_in, hw, nth);
             else
-                nchw_to_nhwc_bf16_v8<float><<<grd, 256, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw,
+                nchw_to_nhwc_bf16_v8<float><<<grd, tpb, 0, st>>>((const float *)x, (__nv_bfloat16 *)xs, s.c_in, hw,
                                                                  nth);
         } else {
             dim3 blk(32, 8), grd((unsigned)ceil_div(hw, 32), (unsigned)ceil_div(s.c_in, 32), (unsigned)s.batch);
