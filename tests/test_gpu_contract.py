@@ -134,6 +134,7 @@ def test_workspace_contract():
     assert v.value == need
 
 
+@pytest.mark.filterwarnings("ignore:The CUDA Graph is empty")  # the refused capture records nothing
 def test_unbuilt_layout_refused_inside_capture():
     """an fp32-prepared layer fed fp64 needs the fp64 direct layout, which prepare did not
     build: inside a capture that is an error, outside it is built once (synchronously)"""
