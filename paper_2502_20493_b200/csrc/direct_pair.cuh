@@ -18,14 +18,18 @@
 
 namespace segb {
 
+#ifndef SEGB_DIRECT_PAIR_PIPE  // double-buffered window loads across input channels
+#define SEGB_DIRECT_PAIR_PIPE 1
+#endif
 struct PairWeights {  // kPairWMax (direct_impl.cuh) floats: a 3.5 KB kernel parameter
     float w[kPairWMax];
 };
 
-template <typename TX, int N, int COB, int RQ, int CQ>
+template <typename TX, int N, int COB, int RQ, int CQ, bool PIPE>
 // (one channel: 2 x 2 quads, 64 live float registers of window and accumulators -> 5 blocks per
-// SM so nothing spills; two: 2 x 1 quads in 80 registers, 6 blocks; three: 4 blocks)
-__global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
+// SM so nothing spills; two: 2 x 1 quads in 80 registers, 6 blocks; three: 4 blocks; PIPE's
+// second window: 4 blocks)
+__global__ void __launch_bounds__(128, PIPE ? 4 : COB == 1 ? 5 : COB == 2 ? 6 : 4)
     direct_pair_kernel(DirectArgs a, const __grid_constant__ PairWeights W) {
     constexpr int NW = N / 2 + 1;    // input rows/cols under one output quad
     constexpr int WR = RQ + NW - 1;  // window rows for RQ row quads
@@ -65,9 +69,7 @@ __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
     for (int j = 0; j < WC; ++j) cok[j] = (unsigned)(col0 + j) < (unsigned)a.w_in;
     const TX *xw = xb + (int64_t)row0 * rs + (int64_t)col0 * es;  // window origin (may point outside)
 
-    float2 win[WR][WC];
-#pragma unroll 1
-    for (int ci = 0; ci < a.c_in; ++ci) {
+    auto load_win = [&](float2 (&win)[WR][WC], int ci) {
         const TX *xc = xw + (int64_t)ci * cs;
         if (warp_inside) {
 #pragma unroll
@@ -88,6 +90,8 @@ __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
                                             (ok && two) ? load_x<TX, float, false>(p + ss) : 0.f);
                 }
         }
+    };
+    auto compute = [&](const float2 (&win)[WR][WC], int ci) {
 #pragma unroll
         for (int c = 0; c < COB; ++c) {
             const float *wv = W.w + (c * a.c_in + ci) * N2P;  // uniform: broadcast operands
@@ -114,6 +118,27 @@ __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
                             fma2(acc[c][2 * qq + 1][2 * cq + 1], win[qq + 1 + u][cq + 1 + v], wv[OFF3 + u * R1 + v]);
                     }
                 }
+        }
+    };
+    float2 wa[WR][WC];
+    if constexpr (PIPE) {
+        // the next channel's window loads in flight while the current one is multiplied (two
+        // window buffers used alternately, no register copies)
+        float2 wb[WR][WC];
+        load_win(wa, 0);
+#pragma unroll 1
+        for (int ci = 0; ci < a.c_in; ci += 2) {
+            if (ci + 1 < a.c_in) load_win(wb, ci + 1);
+            compute(wa, ci);
+            if (ci + 1 >= a.c_in) break;
+            if (ci + 2 < a.c_in) load_win(wa, ci + 2);
+            compute(wb, ci + 1);
+        }
+    } else {
+#pragma unroll 1
+        for (int ci = 0; ci < a.c_in; ++ci) {
+            load_win(wa, ci);
+            compute(wa, ci);
         }
     }
 
@@ -167,7 +192,12 @@ int launch_direct_pair_n(const DirectArgs &a, const PairWeights &W, cudaStream_t
         DirectArgs c = a;
         c.b0 = 2 * p0;
         dim3 grid((unsigned)ceil_div(a.nqc, 32 * CQ), (unsigned)nrb, (unsigned)std::min<int64_t>(65535, pairs - p0));
-        direct_pair_kernel<TX, N, COB, RQ, CQ><<<grid, block, smem, st>>>(c, W);
+        // (measured: three channels ds512_k4_c3 0.302 -> 0.286 ms, n = 5 ds224_k5 0.036 -> 0.034;
+        // one channel with n = 4, ds224_k4, 0.032 -> 0.034: the occupancy it costs is not repaid)
+        if (SEGB_DIRECT_PAIR_PIPE && a.c_in > 1 && (COB == 3 || N == 5))
+            direct_pair_kernel<TX, N, COB, RQ, CQ, true><<<grid, block, smem, st>>>(c, W);
+        else
+            direct_pair_kernel<TX, N, COB, RQ, CQ, false><<<grid, block, smem, st>>>(c, W);
         note_launch();
         if (int rc = check_launch("direct_pair_kernel")) return rc;
     }
