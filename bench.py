@@ -409,7 +409,7 @@ def _max_over_ranks(v, world, dev):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    t = torch.tensor([v], device="cpu" if dist.get_backend() == "gloo" else dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -786,15 +786,22 @@ def main():
         return 2
     if args.impl == "reference":
         return run_reference(args, rank)
+    # SEGB200_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo -- a functional check of the N > 1
+    # path (sharding, barriers, max over ranks, the JSON line) on a one-GPU machine; not a number
+    share = world > 1 and os.environ.get("SEGB200_BENCH_SHARE_GPU") == "1"
+    dev_rank = 0 if share else local_rank
     if world > 1:
         import torch
         import torch.distributed as dist
         os.environ.setdefault("NCCL_DEBUG", "INFO")       # the init log shows nranks / the transport
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(dev_rank)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        return run_ours(args, rank, world, local_rank)
+        return run_ours(args, rank, world, dev_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
