@@ -55,6 +55,12 @@ constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168
 #ifndef SEGB_ROWS_BF16_STCS  // the same for the bf16 epilogue
 #define SEGB_ROWS_BF16_STCS 1  // measured: ebgan_l7 bf16 0.577 -> 0.567 ms
 #endif
+#ifndef SEGB_ROWS_F16_RED  // later channel passes add into y with L2 vector atomics (no read-back)
+#define SEGB_ROWS_F16_RED 1  // measured: ebgan_l6 fp32 0.969 -> 0.938 ms (the add flushes subnormal sums)
+#endif
+__device__ __forceinline__ void red_add_f32x2(float *p, float2 v) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
 #ifndef SEGB_ROWS_F16_STCS
 #define SEGB_ROWS_F16_STCS 1  // measured: ebgan_l7 fp32 1.728 -> 1.681 ms, l6 0.976 -> 0.964
 #endif
@@ -1056,7 +1062,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     for (int h = 0; h < 2; ++h)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)r * prm.ow + h * 32));
             };
-            if (prm.accumulate && t0 < t1) prefetch_tile(t0);
+            if (!SEGB_ROWS_F16_RED && prm.accumulate && t0 < t1) prefetch_tile(t0);
             // the tile's (row i, segment ms, sample b), advanced incrementally (no per-tile divisions)
             int ei = (t0 + toff) % prm.rows, ems = ((t0 + toff) / prm.rows) % prm.msub,
                 eb = ((t0 + toff) / prm.rows) / prm.msub;
@@ -1066,7 +1072,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     ei = 0;
                     if (++ems == prm.msub) { ems = 0; ++eb; }
                 }
-                if (prm.accumulate && t + 1 < t1) prefetch_tile(t + 1);
+                if (!SEGB_ROWS_F16_RED && prm.accumulate && t + 1 < t1) prefetch_tile(t + 1);
                 long long pe_ = clock64();
                 if (warp == kEpiWarp0) { ROWS_PROF(4, pe_) }
                 if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
@@ -1120,7 +1126,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     for (int g8 = 0; g8 < 32; g8 += 8) {
                         if (g8 >= NE) break;
                         float4 old[8];
-                        if (prm.accumulate && lane_active) {
+                        if (!SEGB_ROWS_F16_RED && prm.accumulate && lane_active) {
 #pragma unroll
                             for (int k = 0; k < 8; ++k) {
 #if SEGB_ROWS_F16_ST16
@@ -1152,6 +1158,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                             if (lane_active && !(ABL(1))) {
                                 float2 *d0 = reinterpret_cast<float2 *>(pf + (int64_t)co * plane);
                                 float2 a0 = r0, a1 = r1;
+                                if (SEGB_ROWS_F16_RED && prm.accumulate) {  // y += this pass (one add per element)
+                                    red_add_f32x2(reinterpret_cast<float *>(d0), r0);
+                                    red_add_f32x2(pf + (int64_t)co * plane + prm.ow, r1);
+                                    continue;
+                                }
                                 if (prm.accumulate) {
                                     a0 = make_float2(old[k].x + r0.x, old[k].y + r0.y);
                                     a1 = make_float2(old[k].z + r1.x, old[k].w + r1.y);
