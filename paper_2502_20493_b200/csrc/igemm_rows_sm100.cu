@@ -399,10 +399,14 @@ __device__ __forceinline__ void load_weights(uint8_t *sB, const CUtensorMap *tmB
 // warps store full 32-lane rows.
 // F16 (3xFP16): fp32 input rows are scaled, split into fp16 hi / lo planes by the loaders, the
 // MMA warp issues three MMAs per chunk and the epilogue writes fp32 times 2^-(k_x + k_w).
-template <int NH, int KBC, int SWAP, int MR, int RS, bool F16 = false>
+// FM: 0 = bf16, 1 = 3xFP16 (first channel pass: stores y), 2 = 3xFP16 later pass (adds into y);
+// the pass kind is a template parameter so the storing instance carries no accumulate code
+template <int NH, int KBC, int SWAP, int MR, int RS, int FM = 0>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     igemm_rows_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
                       const RowsParams prm) {
+    constexpr bool F16 = FM != 0;
+    constexpr bool ACCP = FM == 2;  // this launch adds its channel block's sums into y
     constexpr bool TWO = RS == 3 || RS == 4;  // 2-SM pair: M = 128 (RS 3, MR 64) or 256 (RS 4, MR 128)
     constexpr bool COSPLIT = RS == 3;
     // RS = 5 (HALF): one CTA, every tile issued as two row-parity halves (schedules RSEL 0, 1)
@@ -1062,7 +1066,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     for (int h = 0; h < 2; ++h)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)r * prm.ow + h * 32));
             };
-            if (!SEGB_ROWS_F16_RED && prm.accumulate && t0 < t1) prefetch_tile(t0);
+            if (!SEGB_ROWS_F16_RED && ACCP && t0 < t1) prefetch_tile(t0);
             // the tile's (row i, segment ms, sample b), advanced incrementally (no per-tile divisions)
             int ei = (t0 + toff) % prm.rows, ems = ((t0 + toff) / prm.rows) % prm.msub,
                 eb = ((t0 + toff) / prm.rows) / prm.msub;
@@ -1072,7 +1076,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     ei = 0;
                     if (++ems == prm.msub) { ems = 0; ++eb; }
                 }
-                if (!SEGB_ROWS_F16_RED && prm.accumulate && t + 1 < t1) prefetch_tile(t + 1);
+                if (!SEGB_ROWS_F16_RED && ACCP && t + 1 < t1) prefetch_tile(t + 1);
                 long long pe_ = clock64();
                 if (warp == kEpiWarp0) { ROWS_PROF(4, pe_) }
                 if (!(ABL(32))) mbar_wait(&tfull[acc], acc_phase);
@@ -1126,7 +1130,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     for (int g8 = 0; g8 < 32; g8 += 8) {
                         if (g8 >= NE) break;
                         float4 old[8];
-                        if (!SEGB_ROWS_F16_RED && prm.accumulate && lane_active) {
+                        if (!SEGB_ROWS_F16_RED && ACCP && lane_active) {
 #pragma unroll
                             for (int k = 0; k < 8; ++k) {
 #if SEGB_ROWS_F16_ST16
@@ -1150,7 +1154,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                                                            __shfl_xor_sync(0xffffffffu, give.y, 1));
                             float4 v4 = odd ? make_float4(got.x, got.y, r1.x, r1.y) : make_float4(r0.x, r0.y, got.x, got.y);
                             if (lane_active && !(ABL(1))) {
-                                if (prm.accumulate)
+                                if (ACCP)
                                     v4 = make_float4(old[k].x + v4.x, old[k].y + v4.y, old[k].z + v4.z, old[k].w + v4.w);
                                 *reinterpret_cast<float4 *>(pf4 + (int64_t)co * plane) = v4;
                             }
@@ -1158,12 +1162,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                             if (lane_active && !(ABL(1))) {
                                 float2 *d0 = reinterpret_cast<float2 *>(pf + (int64_t)co * plane);
                                 float2 a0 = r0, a1 = r1;
-                                if (SEGB_ROWS_F16_RED && prm.accumulate) {  // y += this pass (one add per element)
+                                if (SEGB_ROWS_F16_RED && ACCP) {  // y += this pass (one add per element)
                                     red_add_f32x2(reinterpret_cast<float *>(d0), r0);
                                     red_add_f32x2(pf + (int64_t)co * plane + prm.ow, r1);
                                     continue;
                                 }
-                                if (prm.accumulate) {
+                                if (ACCP) {
                                     a0 = make_float2(old[k].x + r0.x, old[k].y + r0.y);
                                     a1 = make_float2(old[k].z + r1.x, old[k].w + r1.y);
                                 }
@@ -1191,7 +1195,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                     // CH in flight at once (interleaved with the stores they would be serialised:
                     // the compiler cannot prove the plane-strided addresses distinct)
                     float4 old[CH];
-                    if (prm.accumulate && lane_active) {
+                    if (ACCP && lane_active) {
 #pragma unroll
                         for (int k = 0; k < CH; ++k)
                             old[k] = __ldcs(reinterpret_cast<const float4 *>(pf4 + (int64_t)(co0 + k) * plane));
@@ -1219,7 +1223,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
                         const float4 v4 = odd ? make_float4(got.x, got.y, r1.x, r1.y) : make_float4(r0.x, r0.y, got.x, got.y);
                         if (lane_active && !(ABL(1))) {
                             float4 *dst4 = reinterpret_cast<float4 *>(pf4 + (int64_t)(co0 + k) * plane);
-                            if (prm.accumulate) {  // a later channel pass: y += this pass's sums
+                            if (ACCP) {  // a later channel pass: y += this pass's sums
                                 const float4 o = old[k];
                                 *dst4 = make_float4(o.x + v4.x, o.y + v4.y, o.z + v4.z, o.w + v4.w);
                             } else {
@@ -1469,10 +1473,10 @@ bool igemm_rows_supported(const IgemmShape &s) {
            rows_instantiated(nh, kbc, swap, mr, nsplit, rows_f16(s)) && tensor_map_encoder() != nullptr;
 }
 
-template <int NH, int KBC, int SWAP, int MR, int NS, bool F16 = false>
+template <int NH, int KBC, int SWAP, int MR, int NS, int FM = 0>
 static void launch_rows(int grid, size_t smem, cudaStream_t st, const CUtensorMap &tmB, const CUtensorMap &tmBlo,
                         const RowsParams &prm) {
-    auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS, F16>;
+    auto kern = igemm_rows_kernel<NH, KBC, SWAP, MR, NS, FM>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (NS < 3 || NS == 5) {
         kern<<<grid, kRowsThreads, smem, st>>>(tmB, tmBlo, prm);
@@ -1578,7 +1582,8 @@ int run_igemm_rows(const IgemmShape &s, const void *x, const void *wg, const voi
         for (int ps = 0; ps < passes; ++ps) {
             prm.ch_base = 64 * ps;
             prm.accumulate = ps > 0;
-            launch_rows<2, 1, 0, 64, 3, true>(grid, smem, st, tmB, tmBlo, prm);
+            if (ps == 0) launch_rows<2, 1, 0, 64, 3, 1>(grid, smem, st, tmB, tmBlo, prm);
+            else launch_rows<2, 1, 0, 64, 3, 2>(grid, smem, st, tmB, tmBlo, prm);
             if (ps + 1 < passes) note_launch();
         }
     } else
