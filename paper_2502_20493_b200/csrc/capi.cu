@@ -495,7 +495,9 @@ int segb_describe_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h
     if (pl.path == SEGB_PATH_IGEMM) name = igemm_kernel_name(pl.s);
     else if (use_direct_pair(L, x_dtype, y_dtype, pl.compute))
         name = x_dtype == SEGB_U8_HWC ? "K2p direct (u8 image decoded on load, fp32 FFMA2, two samples per thread)"
-                                      : "K2p direct (fp32 FFMA2, two samples per thread)";
+               : (in_w % 4 == 0 && direct_pair_tma_enabled())
+                   ? "K2p direct (fp32 FFMA2, two samples per thread, TMA-staged input tiles)"
+                   : "K2p direct (fp32 FFMA2, two samples per thread)";
     else if (x_dtype == SEGB_U8_HWC) name = "K2 direct (u8 image decoded on load, fp32 FFMA)";
     else if (pl.compute == SEGB_F64) name = "K2 direct (fp64)";
     else if (pl.compute == SEGB_BF16) name = "K2 direct (bf16 operands, fp32 FFMA)";

@@ -446,6 +446,11 @@ inline bool direct_pair_ok(int c_in, int c_out, int n, int n2p) {
     return c_out >= 1 && c_out <= 3 && n >= 4 && n <= 5 && (int64_t)c_in * c_out * n2p <= kPairWMax;
 }
 int launch_direct_pair_f32(const DirectArgs &a, const float *w_host, cudaStream_t st);
+// fp32 x with W % 4 == 0 runs K2p with TMA-staged input tiles unless SEGB200_DIRECT_PAIR_TMA=0
+inline bool direct_pair_tma_enabled() {
+    const char *e = getenv("SEGB200_DIRECT_PAIR_TMA");
+    return !(e && !atoi(e));
+}
 int launch_direct_pair_u8(const DirectArgs &a, const float *w_host, cudaStream_t st);
 
 }  // namespace segb

@@ -1,5 +1,5 @@
-"""K2p, the paired FFMA2 direct kernel for low-channel fp32 layers (csrc/direct_pair.cuh): bitwise
-equal to K2 (same per-element rule and summation order; SEGB200_DIRECT_PAIR=0 selects K2) over
+"""K2p, the paired FFMA2 direct kernel for low-channel fp32 layers (csrc/direct_pair.cuh; fp32 x with
+W % 4 == 0 takes its TMA-staged variant): bitwise equal to K2 (same per-element rule and summation order; SEGB200_DIRECT_PAIR=0 selects K2) over
 kernel sides (4, 5), paddings (both swap parities), channel counts, odd batches (the last sample
 unpaired), odd and tiny spatial sizes, and within the reference's fp32 gate of the oracle
 (rel 1e-5 / abs 1e-6, /root/reference/pkg/tests/test_acceptance.py:31)."""
@@ -39,6 +39,8 @@ CASES = [  # (batch, c_in, c_out, n, pad, h, w)
     (1, 3, 1, 5, 2, 37, 53), (3, 3, 1, 5, 2, 64, 64), (2, 3, 3, 4, 1, 31, 17), (5, 1, 1, 4, 0, 28, 28),
     (4, 1, 1, 5, 1, 28, 28), (4, 1, 1, 4, 2, 28, 28), (2, 3, 2, 4, 0, 9, 11), (3, 5, 3, 4, 3, 20, 33),
     (2, 7, 1, 5, 4, 16, 16), (7, 3, 1, 4, 2, 1, 1), (2, 3, 3, 5, 2, 66, 130), (6, 2, 2, 5, 3, 5, 40),
+    # W % 4 == 0: the TMA-staged variant, boxes past every edge of small images
+    (2, 3, 1, 5, 3, 5, 4), (3, 2, 2, 4, 1, 3, 8), (1, 3, 3, 5, 0, 9, 12), (5, 1, 1, 4, 2, 20, 132),
 ]
 
 
