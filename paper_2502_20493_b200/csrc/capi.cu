@@ -426,9 +426,10 @@ static int plan_forward(const segb_layer *L, int x_dtype, int64_t batch, int in_
 
 // K2p for the direct path: fp32 compute on f32 / u8-image x into f32 y, the layer's host weight
 // copy made at prepare (SEGB200_DIRECT_PAIR=0 keeps K2, for A/B runs and the bitwise test)
-static bool use_direct_pair(const segb_layer *L, int x_dtype, int y_dtype, int compute) {
+static bool use_direct_pair(const segb_layer *L, int x_dtype, int y_dtype, int compute, int in_w) {
     if (L->w_pair.empty() || compute != SEGB_F32 || y_dtype != SEGB_F32) return false;
     if (x_dtype != SEGB_F32 && x_dtype != SEGB_U8_HWC) return false;
+    if (!direct_pair_n_ok(L->n, x_dtype == SEGB_F32, in_w)) return false;
     const char *e = getenv("SEGB200_DIRECT_PAIR");
     return !(e && !atoi(e));
 }
@@ -470,7 +471,7 @@ static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch
     a.nqc = (ow - 1 + a.swap) / 2 + 1;
     const bool ref = L->engine == SEGB_ENGINE_REFERENCE;
     if (ref) a.p = L->pad;  // the reference engine pads the upsampled map by P
-    if (use_direct_pair(L, x_dtype, y_dtype, compute))
+    if (use_direct_pair(L, x_dtype, y_dtype, compute, in_w))
         return x_dtype == SEGB_U8_HWC ? launch_direct_pair_u8(a, L->w_pair.data(), st)
                                       : launch_direct_pair_f32(a, L->w_pair.data(), st);
     if (x_dtype == SEGB_U8_HWC) return launch_direct_u8(a, ref, st);
@@ -493,7 +494,7 @@ int segb_describe_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h
     if (int rc = plan_forward(L, x_dtype, batch, in_h, in_w, y_dtype, compute, path, pl)) return rc;
     const char *name = "K2 direct (fp32 FFMA)";
     if (pl.path == SEGB_PATH_IGEMM) name = igemm_kernel_name(pl.s);
-    else if (use_direct_pair(L, x_dtype, y_dtype, pl.compute))
+    else if (use_direct_pair(L, x_dtype, y_dtype, pl.compute, in_w))
         name = x_dtype == SEGB_U8_HWC ? "K2p direct (u8 image decoded on load, fp32 FFMA2, two samples per thread)"
                : (in_w % 4 == 0 && direct_pair_tma_enabled())
                    ? "K2p direct (fp32 FFMA2, two samples per thread, TMA-staged input tiles)"

@@ -443,13 +443,18 @@ constexpr int kPairWMax = 896;
 inline bool direct_pair_ok(int c_in, int c_out, int n, int n2p) {
     // n <= 3: K2's one-sample 8 x 4 tiles load fewer window values per output and win (ds224_k3
     // 0.025 vs 0.028 ms); n 4, 5: K2p (ds512_k5 0.150 -> 0.129 ms, ds512_k4_c3 0.351 -> 0.298)
-    return c_out >= 1 && c_out <= 3 && n >= 4 && n <= 5 && (int64_t)c_in * c_out * n2p <= kPairWMax;
+    // (n = 3: only its TMA-staged variant, see direct_pair_n_ok)
+    return c_out >= 1 && c_out <= 3 && n >= 3 && n <= 5 && (int64_t)c_in * c_out * n2p <= kPairWMax;
 }
 int launch_direct_pair_f32(const DirectArgs &a, const float *w_host, cudaStream_t st);
 // fp32 x with W % 4 == 0 runs K2p with TMA-staged input tiles unless SEGB200_DIRECT_PAIR_TMA=0
 inline bool direct_pair_tma_enabled() {
     const char *e = getenv("SEGB200_DIRECT_PAIR_TMA");
     return !(e && !atoi(e));
+}
+// per call: n = 3 only on the TMA-staged variant (the register-window K2p loses to K2 there)
+inline bool direct_pair_n_ok(int n, bool f32_x, int in_w) {
+    return n >= 4 || (f32_x && in_w % 4 == 0 && direct_pair_tma_enabled());
 }
 int launch_direct_pair_u8(const DirectArgs &a, const float *w_host, cudaStream_t st);
 

@@ -377,6 +377,13 @@ int launch_direct_pair_n(const DirectArgs &a, const PairWeights &W, cudaStream_t
     return SEGB_OK;
 }
 
+inline int launch_direct_pair_tma_n3(const DirectArgs &a, const PairWeights &W, cudaStream_t st) {
+    if (a.w_in % 4 != 0) return fail(SEGB_ERR_UNSUPPORTED, "paired direct kernel: n = 3 needs W % 4 == 0");
+    if (a.c_out == 1) return launch_direct_pair_tma_n<3, 1>(a, W, st);
+    if (a.c_out == 2) return launch_direct_pair_tma_n<3, 2>(a, W, st);
+    return launch_direct_pair_tma_n<3, 3>(a, W, st);
+}
+
 template <typename TX, int N>
 int launch_direct_pair_cob(const DirectArgs &a, const PairWeights &W, cudaStream_t st) {
     if constexpr (sizeof(TX) == 4) {  // fp32 NCHW with 16-byte rows: TMA-staged input tiles
@@ -401,6 +408,9 @@ int launch_direct_pair(const DirectArgs &a, const float *w_host, cudaStream_t st
     if (!direct_pair_ok(a.c_in, a.c_out, a.n, a.n2p) || !w_host)
         return fail(SEGB_ERR_UNSUPPORTED, "paired direct kernel: unsupported layer");
     for (int64_t i = 0; i < nw; ++i) W.w[i] = w_host[i];
+    if constexpr (sizeof(TX) == 4) {
+        if (a.n == 3) return launch_direct_pair_tma_n3(a, W, st);
+    }
     if (a.n == 4) return launch_direct_pair_cob<TX, 4>(a, W, st);
     return launch_direct_pair_cob<TX, 5>(a, W, st);
 }

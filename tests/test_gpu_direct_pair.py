@@ -39,8 +39,9 @@ CASES = [  # (batch, c_in, c_out, n, pad, h, w)
     (1, 3, 1, 5, 2, 37, 53), (3, 3, 1, 5, 2, 64, 64), (2, 3, 3, 4, 1, 31, 17), (5, 1, 1, 4, 0, 28, 28),
     (4, 1, 1, 5, 1, 28, 28), (4, 1, 1, 4, 2, 28, 28), (2, 3, 2, 4, 0, 9, 11), (3, 5, 3, 4, 3, 20, 33),
     (2, 7, 1, 5, 4, 16, 16), (7, 3, 1, 4, 2, 1, 1), (2, 3, 3, 5, 2, 66, 130), (6, 2, 2, 5, 3, 5, 40),
-    # W % 4 == 0: the TMA-staged variant, boxes past every edge of small images
+    # W % 4 == 0: the TMA-staged variant, boxes past every edge of small images; n = 3 runs only there
     (2, 3, 1, 5, 3, 5, 4), (3, 2, 2, 4, 1, 3, 8), (1, 3, 3, 5, 0, 9, 12), (5, 1, 1, 4, 2, 20, 132),
+    (3, 1, 1, 3, 0, 28, 28), (4, 1, 1, 3, 1, 28, 28), (2, 3, 2, 3, 2, 30, 36), (3, 3, 3, 3, 3, 7, 8),
 ]
 
 
@@ -66,10 +67,13 @@ def test_pair_dataset_shape_bitwise(torch):
 
 
 def test_pair_not_taken_outside_its_range(torch):
-    """wide layers, n outside 4..5, bf16 compute and the reference engine stay on their kernels"""
-    for c_in, c_out, n, compute in [(3, 4, 4, "fp32"), (3, 1, 7, "fp32"), (3, 1, 3, "fp32"), (3, 1, 5, "bf16")]:
+    """wide layers, n outside 3..5, bf16 compute and the reference engine stay on their kernels"""
+    for c_in, c_out, n, compute in [(3, 4, 4, "fp32"), (3, 1, 7, "fp32"), (3, 1, 5, "bf16")]:
         layer = P.prepare_layer(O.gen_kernel_bank(c_in, c_out, n, 1), 2, compute=compute)
         assert not layer.describe_path(2, 16, 16).startswith("K2p")
+    # n = 3 only on the TMA-staged variant (W % 4 == 0)
+    layer = P.prepare_layer(O.gen_kernel_bank(3, 1, 3, 1), 2)
+    assert layer.describe_path(2, 16, 18).startswith("K2 ") and layer.describe_path(2, 16, 16).startswith("K2p")
     layer = P.prepare_layer(O.gen_kernel_bank(3, 1, 5, 1), 2, engine="reference")
     assert not layer.describe_path(2, 16, 16).startswith("K2p")
 
