@@ -434,6 +434,15 @@ static bool use_direct_pair(const segb_layer *L, int x_dtype, int y_dtype, int c
     return !(e && !atoi(e));
 }
 
+// K2p with shared-memory weights: segregated fp32 layers whose weights exceed the parameter
+static bool use_direct_pair_wsm(const segb_layer *L, int x_dtype, int y_dtype, int compute, int in_w) {
+    if (L->engine != SEGB_ENGINE_SEGREGATED || compute != SEGB_F32 || x_dtype != SEGB_F32 || y_dtype != SEGB_F32)
+        return false;
+    const char *e = getenv("SEGB200_DIRECT_PAIR");
+    if (e && !atoi(e)) return false;
+    return direct_pair_wsm_ok(L->c_in, L->c_out, L->n, L->n2p, in_w);
+}
+
 static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch, int in_h, int in_w, void *y,
                         int y_dtype, int compute, int path, void *ws, int64_t ws_bytes, cudaStream_t st) {
     FwdPlan pl;
@@ -474,6 +483,7 @@ static int forward_impl(segb_layer *L, const void *x, int x_dtype, int64_t batch
     if (use_direct_pair(L, x_dtype, y_dtype, compute, in_w))
         return x_dtype == SEGB_U8_HWC ? launch_direct_pair_u8(a, L->w_pair.data(), st)
                                       : launch_direct_pair_f32(a, L->w_pair.data(), st);
+    if (use_direct_pair_wsm(L, x_dtype, y_dtype, compute, in_w)) return launch_direct_pair_wsm(a, st);
     if (x_dtype == SEGB_U8_HWC) return launch_direct_u8(a, ref, st);
     switch (compute) {
         case SEGB_F32:
@@ -499,6 +509,8 @@ int segb_describe_path(const segb_layer *L, int x_dtype, int64_t batch, int in_h
                : (in_w % 4 == 0 && direct_pair_tma_enabled())
                    ? "K2p direct (fp32 FFMA2, two samples per thread, TMA-staged input tiles)"
                    : "K2p direct (fp32 FFMA2, two samples per thread)";
+    else if (pl.path == SEGB_PATH_DIRECT && use_direct_pair_wsm(L, x_dtype, y_dtype, pl.compute, in_w))
+        name = "K2p direct (fp32 FFMA2, two samples per thread, TMA-staged input tiles, weights in shared memory)";
     else if (x_dtype == SEGB_U8_HWC) name = "K2 direct (u8 image decoded on load, fp32 FFMA)";
     else if (pl.compute == SEGB_F64) name = "K2 direct (fp64)";
     else if (pl.compute == SEGB_BF16) name = "K2 direct (bf16 operands, fp32 FFMA)";

@@ -9,4 +9,5 @@ int launch_direct_f32(const DirectArgs &a, bool ref_engine, cudaStream_t st) {
 int launch_direct_pair_f32(const DirectArgs &a, const float *w_host, cudaStream_t st) {
     return launch_direct_pair<float>(a, w_host, st);
 }
+int launch_direct_pair_wsm(const DirectArgs &a, cudaStream_t st) { return launch_direct_pair_wsm_impl(a, st); }
 }  // namespace segb

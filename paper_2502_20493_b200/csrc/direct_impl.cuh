@@ -452,6 +452,14 @@ inline bool direct_pair_tma_enabled() {
     const char *e = getenv("SEGB200_DIRECT_PAIR_TMA");
     return !(e && !atoi(e));
 }
+// K2p with the weights in shared memory (TMA-staged input; the layer's K2 weights a.w): fp32 x,
+// W % 4 == 0, c_out <= 3, n 3..5, more weights than the kernel parameter holds, <= 12 K floats
+inline bool direct_pair_wsm_ok(int c_in, int c_out, int n, int n2p, int in_w) {
+    const int64_t nw = (int64_t)c_in * c_out * n2p;
+    return c_out >= 1 && c_out <= 3 && n >= 3 && n <= 5 && nw > kPairWMax && nw <= 12288 && in_w % 4 == 0 &&
+           direct_pair_tma_enabled();
+}
+int launch_direct_pair_wsm(const DirectArgs &a, cudaStream_t st);
 // per call: n = 3 only on the TMA-staged variant (the register-window K2p loses to K2 there)
 inline bool direct_pair_n_ok(int n, bool f32_x, int in_w) {
     return n >= 4 || (f32_x && in_w % 4 == 0 && direct_pair_tma_enabled());

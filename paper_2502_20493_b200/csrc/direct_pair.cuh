@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(128, PIPE ? 4 : COB == 1 ? 5 : COB == 2 ? 6 : 
 // memory, double-buffered across channels and zero-filled outside the image (no predicated
 // loads); threads read their register windows from shared memory. Same rule, order and bits as
 // K2p / K2.
-template <int N, int COB, int RQ, int CQ, int TR, int TC>
+// WSM: the weights (too many for the kernel parameter, e.g. dcgan_l5: 128 x 3 x 16) are copied
+// from a.w into shared memory at block start and read as broadcast loads
+template <int N, int COB, int RQ, int CQ, int TR, int TC, bool WSM = false>
 __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
     direct_pair_tma_kernel(const __grid_constant__ CUtensorMap tmX, DirectArgs a, const __grid_constant__ PairWeights W) {
     constexpr int NW = N / 2 + 1;
@@ -202,6 +204,13 @@ __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + 2 * TILE * sizeof(float));   // 2 barriers
     float *stg_base = reinterpret_cast<float *>(smem_raw + 2 * TILE * sizeof(float) + 64);
     const int tid = threadIdx.y * 32 + threadIdx.x;
+    // WSM: the weights after the store staging area
+    float *sW = stg_base + kDirectRowsPerBlock * COB * 2 * RQ * 64 * CQ;
+    if constexpr (WSM) {
+        const int nw4 = COB * a.c_in * N2P / 4;  // N2P % 4 == 0
+        const float4 *src = reinterpret_cast<const float4 *>(a.w);
+        for (int i = tid; i < nw4; i += blockDim.x * blockDim.y) reinterpret_cast<float4 *>(sW)[i] = __ldg(src + i);
+    }
     const int qb = blockIdx.y * kDirectRowsPerBlock * RQ, tb = blockIdx.x * 32 * CQ;  // block's first quads
     const int q0 = qb + threadIdx.y * RQ;
     const int64_t b = a.b0 + 2 * (int64_t)blockIdx.z;
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
         if (tid == 0 && ci + 2 < a.c_in) issue(ci + 2);
 #pragma unroll
         for (int c = 0; c < COB; ++c) {
-            const float *wv = W.w + (c * a.c_in + ci) * N2P;
+            const float *wv = (WSM ? sW : W.w) + (c * a.c_in + ci) * N2P;
             auto fma2 = [&](float2 &d, const float2 &x, float w) { d = __ffma2_rn(x, make_float2(w, w), d); };
 #pragma unroll
             for (int qq = 0; qq < RQ; ++qq)
@@ -315,7 +324,7 @@ __global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
 #define SEGB_DIRECT_PAIR_TMA 1
 #endif
 
-template <int N, int COB>
+template <int N, int COB, bool WSM = false>
 int launch_direct_pair_tma_n(const DirectArgs &a, const PairWeights &W, cudaStream_t st) {
     constexpr int RQ = 2, CQ = COB == 1 ? 2 : 1;
     constexpr int NW = N / 2 + 1;
@@ -337,8 +346,9 @@ int launch_direct_pair_tma_n(const DirectArgs &a, const PairWeights &W, cudaStre
     const int64_t nrb = ceil_div(a.nqr, kDirectRowsPerBlock * RQ);
     if (nrb > 65535) return fail(SEGB_ERR_UNSUPPORTED, "output too large for the paired direct kernel grid");
     const size_t smem = 128 + 2 * ((2 * TR * TC + 31) / 32 * 32) * sizeof(float) + 64 +
-                        sizeof(float) * kDirectRowsPerBlock * COB * 2 * RQ * 64 * CQ;
-    auto kern = direct_pair_tma_kernel<N, COB, RQ, CQ, TR, TC>;
+                        sizeof(float) * kDirectRowsPerBlock * COB * 2 * RQ * 64 * CQ +
+                        (WSM ? sizeof(float) * COB * a.c_in * a.n2p : 0);
+    auto kern = direct_pair_tma_kernel<N, COB, RQ, CQ, TR, TC, WSM>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t pairs = ceil_div(a.batch, 2);
     for (int64_t p0 = 0; p0 < pairs; p0 += 65535) {
@@ -375,6 +385,21 @@ int launch_direct_pair_n(const DirectArgs &a, const PairWeights &W, cudaStream_t
         if (int rc = check_launch("direct_pair_kernel")) return rc;
     }
     return SEGB_OK;
+}
+
+// fp32 x, W % 4 == 0, n 3..5, c_out <= 3, weights too many for the parameter (direct_pair_wsm_ok):
+// the TMA-staged kernel with its weights in shared memory, read from the layer's K2 weights (a.w)
+template <int N>
+int launch_direct_pair_wsm_n(const DirectArgs &a, cudaStream_t st) {
+    static PairWeights unused{};  // (the parameter slot the WSM instance does not read)
+    if (a.c_out == 1) return launch_direct_pair_tma_n<N, 1, true>(a, unused, st);
+    if (a.c_out == 2) return launch_direct_pair_tma_n<N, 2, true>(a, unused, st);
+    return launch_direct_pair_tma_n<N, 3, true>(a, unused, st);
+}
+inline int launch_direct_pair_wsm_impl(const DirectArgs &a, cudaStream_t st) {
+    if (a.n == 3) return launch_direct_pair_wsm_n<3>(a, st);
+    if (a.n == 4) return launch_direct_pair_wsm_n<4>(a, st);
+    return launch_direct_pair_wsm_n<5>(a, st);
 }
 
 inline int launch_direct_pair_tma_n3(const DirectArgs &a, const PairWeights &W, cudaStream_t st) {

@@ -92,3 +92,24 @@ def test_pair_writes_exactly_the_output(torch, batch, c_in, c_out, n, pad, h, w)
     torch.cuda.synchronize()
     assert not torch.isnan(y).any()
     assert torch.isnan(buf[:guard]).all() and torch.isnan(buf[guard + count:]).all()
+
+
+@pytest.mark.parametrize("batch,c_in,c_out,n,pad,h,w", [(2, 128, 3, 4, 2, 32, 32), (3, 96, 2, 5, 1, 12, 20),
+                                                         (4, 200, 1, 3, 3, 9, 16)])
+def test_pair_weights_in_shared_memory(torch, batch, c_in, c_out, n, pad, h, w):
+    """more weights than the kernel parameter holds (dcgan_l5: 128 x 3 x 16): the TMA-staged K2p
+    reads them from shared memory; bitwise K2 and within the oracle's gate"""
+    bank = O.gen_kernel_bank(c_in, c_out, n, 21 + n)
+    layer = P.prepare_layer(bank, pad)
+    x = torch.from_numpy(O.unit_floats(batch * c_in * h * w, 3 + h).reshape(batch, c_in, h, w)).cuda()
+    assert "weights in shared memory" in layer.describe_path(batch, h, w, path="direct")
+    y_pair = layer.forward(x, path="direct")
+    os.environ["SEGB200_DIRECT_PAIR"] = "0"
+    try:
+        y_k2 = layer.forward(x, path="direct")
+    finally:
+        del os.environ["SEGB200_DIRECT_PAIR"]
+    assert torch.equal(y_pair, y_k2)
+    ref = O.forward_segregated_batch(x.cpu().numpy().astype(np.float64), bank.astype(np.float64), pad)
+    assert O.compare(y_pair.cpu().numpy(), ref, 1e-5, 1e-6)["passed"]
+
