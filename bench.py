@@ -631,10 +631,13 @@ def measure(args, workload, rank, world, local_rank, with_e2e=True, with_memory=
         d2h = sum(t.numel() * t.element_size() for t in hy)
 
         def e2e_step():
-            # every layer through the public API with host tensors; the D2H copies stay in flight
-            # (non_blocking) and the region ends with a synchronize
+            # every layer through the public API with host tensors; each layer's D2H copies stay in
+            # flight (non_blocking) while the next layer's input copies and kernels run, and the step
+            # ends with the stream ordered after all of them (wait_host_copies), so the closing event
+            # counts every byte
             for s, xi, yi in zip(state, hx, hy):
                 s["layer"].forward(xi, out=yi, non_blocking=True)
+            P.wait_host_copies(dev)
 
         e2e_step()
         torch.cuda.synchronize()

@@ -19,6 +19,7 @@ from .engines import (
     transpose_conv_reference,
     transpose_conv_reference_counted,
     transpose_conv_segregated,
+    wait_host_copies,
     transpose_conv_segregated_counted,
 )
 from .errors import ShapeError, SpecError
@@ -42,4 +43,5 @@ __all__ = [
     "mult_count_segregated", "output_dims", "prepare_layer", "prepare_stack", "segregate_kernel",
     "subkernel_dims", "transpose_conv_reference", "transpose_conv_reference_counted",
     "transpose_conv_segregated", "transpose_conv_segregated_counted",
+    "wait_host_copies",
 ]

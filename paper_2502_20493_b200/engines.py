@@ -55,6 +55,19 @@ def _copy_streams(dev):
     return _COPY_STREAMS[key]
 
 
+def wait_host_copies(device=None):
+    """Orders the current stream of `device` after every host copy that forwards with
+    `non_blocking=True` left in flight (the pipelined host path's copy streams); after it, an event
+    recorded on the current stream marks those copies complete."""
+    t = _device.torch()
+    dev = t.device("cuda", t.cuda.current_device()) if device is None else t.device(device)
+    key = str(dev)
+    if key in _COPY_STREAMS:
+        cur = t.cuda.current_stream(dev)
+        for s in _COPY_STREAMS[key]:
+            cur.wait_stream(s)
+
+
 @dataclass(frozen=True)
 class ComparisonReport:
     """Element-wise agreement between two tensors (the second one is the reference)."""
@@ -206,7 +219,9 @@ class PreparedLayer:
         """engines.py:246-256. numpy (C,H,W) in -> numpy out (dtype = result_type of
         x and bank, as the reference); torch in -> torch out. A host `out=` tensor is complete
         when forward returns (the reference returns finished host arrays); `non_blocking=True`
-        leaves that device-to-host copy in flight on the caller's current stream instead."""
+        leaves that device-to-host copy in flight instead: on the caller's current stream, or -- for a
+        pipelined host batch -- on the layer's copy stream, so the next call's input copies and kernels
+        overlap it; `wait_host_copies()` (or a synchronize) orders the caller after it."""
         x = require_channel_tensor(x)
         c_axis = 1 if (_is_torch(x) and x.dim() == 4) else 0
         if x.shape[c_axis] != self.c_in:
@@ -219,7 +234,7 @@ class PreparedLayer:
         if path not in _lib.PATH_IDS:
             raise ValueError(f"unknown path {path!r}, expected one of {tuple(_lib.PATH_IDS)}")
         if _is_torch(x):
-            y = self._forward_torch(x, out, path, out_dtype, out_h, out_w)
+            y = self._forward_torch(x, out, path, out_dtype, out_h, out_w, in_flight=non_blocking)
             if out is not None and not out.is_cuda and not non_blocking:
                 _device.torch().cuda.current_stream(self.device).synchronize()
             return y
@@ -244,7 +259,7 @@ class PreparedLayer:
         self._launch(d_x, d_y, compute, path)
         return d_y[0].cpu().numpy().astype(dt, copy=False)
 
-    def _forward_torch(self, x, out, path, out_dtype, out_h, out_w):
+    def _forward_torch(self, x, out, path, out_dtype, out_h, out_w, in_flight=False):
         t = _device.torch()
         squeeze = x.dim() == 3
         xb = x[None] if squeeze else x
@@ -252,7 +267,8 @@ class PreparedLayer:
         if (host_in and xb.shape[0] >= 2 and (out is None or not out.is_cuda)
                 and xb.numel() * xb.element_size() >= _PIPELINE_MIN_BYTES):
             y = self._forward_host_pipelined(xb, None if out is None else out.view(
-                (xb.shape[0], self.c_out, out_h, out_w)), path, out_dtype, out_h, out_w)
+                (xb.shape[0], self.c_out, out_h, out_w)), path, out_dtype, out_h, out_w,
+                in_flight=in_flight and out is not None)
             if out is not None:
                 return out
             return y[0] if squeeze else y
@@ -287,7 +303,7 @@ class PreparedLayer:
             return (d_y[0] if squeeze else d_y).to("cpu")
         return d_y[0] if squeeze else d_y
 
-    def _forward_host_pipelined(self, xh, out_h_t, path, out_dtype, out_h, out_w):
+    def _forward_host_pipelined(self, xh, out_h_t, path, out_dtype, out_h, out_w, in_flight=False):
         """Host (pinned) batch in, host batch out, as a 3-stage pipeline over batch chunks:
         the H2D copy of chunk k+1 (copy stream), the kernels of chunk k (caller's stream) and
         the D2H copy of chunk k-1 (second copy stream) overlap, so PCIe runs both directions at
@@ -354,7 +370,8 @@ class PreparedLayer:
             buf.record_stream(h2d)
         for buf in yout:
             buf.record_stream(d2h)
-        main.wait_event(last)
+        if not in_flight:  # (in flight: wait_host_copies() orders the caller after the copies)
+            main.wait_event(last)
         main.wait_event(in_ready)
         if returned:
             main.synchronize()

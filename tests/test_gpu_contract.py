@@ -163,3 +163,23 @@ def test_host_out_is_complete_on_return():
         layer.forward(x, out=host)
         assert not torch.isnan(host).any()  # read right away, no synchronize
     assert torch.equal(host, layer.forward(x).cpu())
+
+
+def test_in_flight_host_copies_then_wait():
+    """non_blocking host outputs of consecutive pipelined forwards: the copies overlap the next
+    call; after wait_host_copies() and a synchronize every output is complete and equal to the
+    blocking result"""
+    import torch
+    layer, x = _layer_and_input("K3b bf16")
+    xh = torch.cat([x] * 4).cpu().pin_memory()  # a batch the host pipeline takes
+    oh, ow = layer.output_shape(64, 64)
+    outs = [torch.full((xh.shape[0], 64, oh, ow), float("nan"), dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    for o in outs:
+        layer.forward(xh, out=o, non_blocking=True)
+    P.wait_host_copies(x.device)
+    done = torch.cuda.Event()
+    done.record()
+    done.synchronize()
+    ref = layer.forward(xh)
+    for o in outs:
+        assert torch.equal(o, ref)
