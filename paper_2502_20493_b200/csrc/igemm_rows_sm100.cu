@@ -58,6 +58,8 @@ constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168
 #ifndef SEGB_ROWS_F16_RED  // later channel passes add into y with L2 vector atomics (no read-back)
 #define SEGB_ROWS_F16_RED 1  // measured: ebgan_l6 fp32 0.969 -> 0.938 ms (the add flushes subnormal sums)
 #endif
+// (the 16-byte store variant, SEGB_ROWS_F16_ST16, keeps the read-modify-write accumulation)
+static_assert(!(SEGB_ROWS_F16_ST16 && SEGB_ROWS_F16_RED), "SEGB_ROWS_F16_ST16 needs SEGB_ROWS_F16_RED=0");
 __device__ __forceinline__ void red_add_f32x2(float *p, float2 v) {
     asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
