@@ -58,8 +58,6 @@ constexpr int kRegsCtl = 96, kRegsLoad = 232;                 // 128 x (96 + 168
 #ifndef SEGB_ROWS_F16_RED  // later channel passes add into y with L2 vector atomics (no read-back)
 #define SEGB_ROWS_F16_RED 1  // measured: ebgan_l6 fp32 0.969 -> 0.938 ms (the add flushes subnormal sums)
 #endif
-// (the 16-byte store variant, SEGB_ROWS_F16_ST16, keeps the read-modify-write accumulation)
-static_assert(!(SEGB_ROWS_F16_ST16 && SEGB_ROWS_F16_RED), "SEGB_ROWS_F16_ST16 needs SEGB_ROWS_F16_RED=0");
 __device__ __forceinline__ void red_add_f32x2(float *p, float2 v) {
     asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -69,6 +67,8 @@ __device__ __forceinline__ void red_add_f32x2(float *p, float2 v) {
 #ifndef SEGB_ROWS_F16_ST16  // 3xFP16 epilogue stores: 16-byte (lane-pair exchange) or two 8-byte per channel
 #define SEGB_ROWS_F16_ST16 0  // measured: 8-byte stores without exchange -3.5% (l7), -8% (l6) vs 16-byte
 #endif
+// (the 16-byte store variant keeps the read-modify-write accumulation)
+static_assert(!(SEGB_ROWS_F16_ST16 && SEGB_ROWS_F16_RED), "SEGB_ROWS_F16_ST16 needs SEGB_ROWS_F16_RED=0");
 constexpr int kRegsLoadF16 = 192, kRegsEpiF16 = 216;          // 128 x (96 + 216 + 192) <= 128 x 3 x 168
 constexpr int kRingMax = 8;         // input-row slots: as many as shared memory holds, <= 8
 // 3xFP16 loaders hand each filled slot to an "arriver" warp (warp 2) through a named barrier;
