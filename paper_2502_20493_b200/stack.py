@@ -18,7 +18,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _device, _lib
-from .engines import COMPUTE_DTYPES, PreparedLayer, _is_torch
+from .engines import _PIPELINE_CHUNKS, _PIPELINE_MIN_BYTES, COMPUTE_DTYPES, PreparedLayer, _copy_streams, _is_torch
 from .errors import ShapeError
 
 
@@ -76,6 +76,76 @@ class PreparedStack:
             self._ws[key] = t.empty(max(1, nbytes), dtype=t.uint8, device=self.device)
         return self._ws[key]
 
+    def _chunk_graph(self, n, h, w, x_dtype, out_dtype, slot):
+        """The chain over an n-sample chunk as a captured graph on static buffers (one per slot)."""
+        t = _device.torch()
+        key = ("chunk", n, h, w, x_dtype, out_dtype, slot)
+        if key not in self._graphs:
+            oh, ow = self.output_shape(h, w)
+            sx = t.zeros((n, self.c_in, h, w), dtype=x_dtype, device=self.device)
+            sy = t.empty((n, self.c_out, oh, ow), dtype=out_dtype, device=self.device)
+            self._launch(sx, sy)  # warm-up outside the capture
+            t.cuda.current_stream(self.device).synchronize()
+            g = t.cuda.CUDAGraph()
+            with t.cuda.graph(g):
+                self._launch(sx, sy)
+            self._graphs[key] = (g, sx, sy)
+        return self._graphs[key]
+
+    def _pipeline_chunk(self, b, h, w, x_dtype, out_dtype):
+        """A chunk size for the host pipeline: a divisor of the batch (b / 8, / 4 or / 2) whose
+        every layer dispatches exactly as the whole batch does (same kernel and tile configuration,
+        hence the same bits per sample), else 0 (no chunking)."""
+        t = _device.torch()
+        inter = {"bf16": t.bfloat16, "fp32": t.float32, "fp64": t.float64}[self.inter_dtype]
+        for nch in (_PIPELINE_CHUNKS, 4, 2):
+            if b % nch or b // nch < 2:
+                continue
+            cs = b // nch
+            ok, hi, wi = True, h, w
+            for i, L in enumerate(self.layers):
+                xd = x_dtype if i == 0 else inter
+                yd = out_dtype if i == len(self.layers) - 1 else inter
+                if L.describe_path(cs, hi, wi, xd, yd) != L.describe_path(b, hi, wi, xd, yd):
+                    ok = False
+                    break
+                hi, wi = L.output_shape(hi, wi)
+            if ok:
+                return cs
+        return 0
+
+    def _forward_host_pipelined(self, xh, out_h, out_dtype, h, w, cs):
+        """Host batch in, host batch out, over batch chunks of cs samples: chunk k's chain (one
+        graph replay, its input copied in first) runs while chunk k-1's output is copied out on the
+        copy stream (two output buffers in rotation). Every chunk dispatches as the whole batch
+        (_pipeline_chunk), so the result is the whole-batch chain's, bitwise."""
+        t = _device.torch()
+        main = t.cuda.current_stream(self.device)
+        d2h = _copy_streams(self.device)[1]
+        b = int(xh.shape[0])
+        out_free = [None, None]
+        last = None
+        start = t.cuda.Event()
+        start.record(main)
+        d2h.wait_event(start)
+        for k, a in enumerate(range(0, b, cs)):
+            e = min(b, a + cs)
+            slot = k % 2
+            g, sx, sy = self._chunk_graph(e - a, h, w, xh.dtype, out_dtype, slot)
+            if out_free[slot] is not None:
+                main.wait_event(out_free[slot])  # the copy-out of this buffer's previous chunk
+            sx.copy_(xh[a:e], non_blocking=True)
+            g.replay()
+            done = t.cuda.Event()
+            done.record(main)
+            with t.cuda.stream(d2h):
+                d2h.wait_event(done)
+                out_h[a:e].copy_(sy, non_blocking=True)
+                last = t.cuda.Event()
+                last.record(d2h)
+            out_free[slot] = last
+        main.wait_event(last)
+
     def _launch(self, d_x, d_y):
         b, _, h, w = d_x.shape
         ws = self._workspace(int(b), int(h), int(w), d_x.dtype, d_y.dtype)
@@ -109,6 +179,13 @@ class PreparedStack:
                              f"{tuple(out.shape)} {out.dtype}")
         host_in = not xb.is_cuda
         host_out = out is not None and not out.is_cuda
+        cs = (self._pipeline_chunk(b, h, w, xb.dtype, out_dtype) if (
+            host_in and host_out and self.graph and b * self.c_out * oh * ow * out.element_size() >= _PIPELINE_MIN_BYTES)
+              else 0)
+        if cs:
+            self._forward_host_pipelined(xb, out.view(shape), out_dtype, h, w, cs)
+            t.cuda.current_stream(self.device).synchronize()
+            return out
         if host_in and self.graph:
             # host batch: one H2D into a static device input, the chain replayed as one
             # captured graph, one D2H of the final output

@@ -67,6 +67,27 @@ def test_bf16_stack_host_batch_graph_replay():
     assert torch.equal(stack.forward(xh), want)  # host in -> host tensor out
 
 
+def test_stack_host_batch_chunk_pipeline():
+    """a host batch whose output is large enough for the chunked pipeline (copy-out of chunk k-1
+    beside the chain of chunk k; chunks that dispatch as the whole batch): bitwise the whole-batch
+    device chain"""
+    import torch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    layers = [P.prepare_layer(O.gen_kernel_bank(ci, co, n, 41 + i), pad, compute="bf16")
+              for i, (ci, co, n, pad) in enumerate(BF16_STACK[:3])]
+    stack = P.prepare_stack(layers)
+    xd = device_unit_floats((64, 256, 8, 8), 13, dtype=torch.bfloat16)
+    want = stack.forward(xd).cpu()
+    xh = xd.cpu().pin_memory()
+    oh = torch.empty(tuple(want.shape), dtype=want.dtype).pin_memory()
+    for _ in range(2):
+        oh.fill_(float("nan"))
+        stack.forward(xh, out=oh)
+        assert torch.equal(oh, want)
+    assert stack._pipeline_chunk(64, 8, 8, torch.bfloat16, torch.bfloat16) > 0
+    assert any(k[0] == "chunk" for k in stack._graphs)
+
+
 def test_fp32_stack_matches_oracle_chain():
     """low-channel fp32 chain on the direct kernel, odd kernels and an odd P (the swap)"""
     import torch
