@@ -303,12 +303,27 @@ class PreparedLayer:
             return (d_y[0] if squeeze else d_y).to("cpu")
         return d_y[0] if squeeze else d_y
 
+    def _pipeline_chunk(self, b, h, w, x_dtype, y_dtype, compute, path):
+        """Chunk size of the host pipeline: b / 8, / 4 or / 2 (rounded up), the first whose chunk
+        sizes all dispatch exactly as the whole batch (same kernel and tile configuration, so the
+        same bits per sample: the dispatch adapts to the batch, e.g. split K for small ones), else
+        the whole batch as one chunk."""
+        whole = self.describe_path(b, h, w, x_dtype, y_dtype, compute, path)
+        for nch in (_PIPELINE_CHUNKS, 4, 2):
+            cs = (b + nch - 1) // nch
+            if cs < 1 or cs >= b:
+                continue
+            sizes = {cs, b - cs * ((b - 1) // cs)}
+            if all(self.describe_path(n, h, w, x_dtype, y_dtype, compute, path) == whole for n in sizes):
+                return cs
+        return b
+
     def _forward_host_pipelined(self, xh, out_h_t, path, out_dtype, out_h, out_w, in_flight=False):
         """Host (pinned) batch in, host batch out, as a 3-stage pipeline over batch chunks:
         the H2D copy of chunk k+1 (copy stream), the kernels of chunk k (caller's stream) and
         the D2H copy of chunk k-1 (second copy stream) overlap, so PCIe runs both directions at
-        once instead of copy-in / compute / copy-out in series. Samples are independent, so
-        the result is bitwise that of one whole-batch call. Ordered after prior work on the
+        once instead of copy-in / compute / copy-out in series. The chunks dispatch as the whole
+        batch does (_pipeline_chunk), so the result is bitwise that of one whole-batch call. Ordered after prior work on the
         caller's current stream, which waits for the last copy before returning; a returned
         (not `out=`) tensor is complete on return, as `.to("cpu")` would be."""
         t = _device.torch()
@@ -330,8 +345,7 @@ class PreparedLayer:
             raise ShapeError(f"out must be a contiguous {shape} tensor, got {tuple(out_h_t.shape)}")
         elif out_h_t.dtype != out_dtype:
             raise ValueError(f"out dtype {out_h_t.dtype} != {out_dtype}")
-        nchunk = min(b, _PIPELINE_CHUNKS)
-        cs = (b + nchunk - 1) // nchunk
+        cs = self._pipeline_chunk(b, xh.shape[-2], xh.shape[-1], dev_in_dt, out_dtype, compute, path)
         spans = [(i, min(b, i + cs)) for i in range(0, b, cs)]
         xin = [t.empty((cs,) + tuple(xh.shape[1:]), dtype=xh.dtype, device=dev) for _ in range(2)]
         yout = [t.empty((cs,) + shape[1:], dtype=out_dtype, device=dev) for _ in range(2)]
