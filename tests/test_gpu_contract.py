@@ -183,3 +183,22 @@ def test_in_flight_host_copies_then_wait():
     ref = layer.forward(xh)
     for o in outs:
         assert torch.equal(o, ref)
+
+
+@pytest.mark.parametrize("ci,co,h,batch,compute", [(2048, 1024, 4, 64, "fp32"), (1024, 512, 4, 96, "bf16"),
+                                                    (64, 64, 128, 6, "fp32")])
+def test_host_pipeline_bitwise_whole_batch(ci, co, h, batch, compute):
+    """the pipelined host path picks chunks that dispatch as the whole batch: bitwise the
+    device-resident whole-batch forward (ebgan_l2-like layers change tile configuration at
+    small batches)"""
+    import torch
+    from paper_2502_20493_b200.synth import device_unit_floats
+    tdt = torch.bfloat16 if compute == "bf16" else torch.float32
+    layer = P.prepare_layer(device_unit_floats((ci, co, 4, 4), 3), 2, compute=compute)
+    xd = device_unit_floats((batch, ci, h, h), 4, dtype=tdt)
+    want = layer.forward(xd).cpu()
+    xh = xd.cpu().pin_memory()
+    oh, ow = layer.output_shape(h, h)
+    out = torch.empty((batch, co, oh, ow), dtype=want.dtype).pin_memory()
+    layer.forward(xh, out=out)
+    assert torch.equal(out, want)
