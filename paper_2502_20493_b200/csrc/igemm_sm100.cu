@@ -823,8 +823,14 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     {  // few position blocks (small batches: DCGAN/EB-GAN l2 at batch 1 has 16 positions per class):
        // narrower N tiles until the four classes' tiles cover the SMs, so the weight stream -- the
        // bytes that bound such a layer -- is read by many SMs at once instead of a handful
+        // (2-SM pairs from two position tiles on: count pair tiles against half the 74 pairs -- a
+        // wider N tile with most pairs busy beats twice the tiles at half the width: dcgan_l2 at
+        // batch 64, N 64 -> 128: 0.040 -> 0.030 ms; dcgan_l3, N 128 -> 256: 0.031 -> 0.028)
         const int64_t mt = ceil_div(s.batch * (int64_t)((oh + 1) / 2) * ((ow + 1) / 2), kBlockM);
-        while (nt > 32 && nt % 64 == 0 && cop % (nt / 2) == 0 && 4 * mt * (cop / nt) < 148) nt /= 2;
+        const bool pairs = mt >= 2;
+        auto units = [&](int n) { return pairs ? 4 * ((mt + 1) / 2) * (cop / n) : 4 * mt * (cop / n); };
+        const int64_t target = pairs ? 37 : 148;
+        while (nt > 32 && nt % 64 == 0 && cop % (nt / 2) == 0 && units(nt) < target) nt /= 2;
     }
     if (const char *e = getenv("SEGB200_K3_NTILE")) {  // A/B experiments: force the N tile
         const int v = atoi(e);
