@@ -817,9 +817,8 @@ static bool make_params(const IgemmShape &s, IgemmParams &prm) {
     if (!nt)
         for (int cand : {256, 128, 64, 32})
             if (cand <= nmax && cop % cand == 0) { nt = cand; break; }
-    // 1024+ output channels: N = 128 tiles quantise better over the SMs (ebgan_l2 0.195 -> 0.190
-    // ms); with fewer channels the halved N re-reads A twice as often and loses (dcgan l2-l4)
-    if (!tf32 && cop >= 1024 && cop % 128 == 0) nt = 128;
+    // (round 1 used N = 128 for 1024+ output channels; with the current pipeline N = 256 is
+    // faster there too: ebgan_l2 bf16 0.222 -> 0.193 ms)
     {  // few position blocks (small batches: DCGAN/EB-GAN l2 at batch 1 has 16 positions per class):
        // narrower N tiles until the four classes' tiles cover the SMs, so the weight stream -- the
        // bytes that bound such a layer -- is read by many SMs at once instead of a handful
