@@ -654,7 +654,10 @@ __global__ void nchw_to_nhwc_tf32x2(const float *__restrict__ x, float *__restri
 // input's absmax partials, f16split.cuh). Each thread (staging_tile) loads an 8-channel x
 // 8-position tile with 128-bit loads, splits it and transposes the fp16 pairs
 // in registers (byte permutes) into 8 channels-last 16-byte rows per plane. HW % 8 == 0, C % 8 == 0.
-__global__ void __launch_bounds__(256) nchw_to_nhwc_f16x2_v8(const float *__restrict__ x, __half *__restrict__ hi,
+#ifndef SEGB_STAGING_MINB  // four 256-thread blocks per SM (<= 64 registers): ebgan_l5 fp32 0.767 -> 0.712 ms,
+#define SEGB_STAGING_MINB 4   // l4 0.628 -> 0.601 (six blocks spill and lose)
+#endif
+__global__ void __launch_bounds__(256, SEGB_STAGING_MINB) nchw_to_nhwc_f16x2_v8(const float *__restrict__ x, __half *__restrict__ hi,
                                                               __half *__restrict__ lo, int C, int HW, int64_t nthreads,
                                                               const float *__restrict__ partials) {
     __shared__ float scale;
