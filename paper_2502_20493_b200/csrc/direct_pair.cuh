@@ -187,8 +187,11 @@ __global__ void __launch_bounds__(128, PIPE ? 4 : COB == 1 ? 5 : COB == 2 ? 6 : 
 // K2p / K2.
 // WSM: the weights (too many for the kernel parameter, e.g. dcgan_l5: 128 x 3 x 16) are copied
 // from a.w into shared memory at block start and read as broadcast loads
+#ifndef SEGB_PAIR_TMA_MINB1  // blocks per SM of the one-channel TMA-staged kernel
+#define SEGB_PAIR_TMA_MINB1 6  // measured: ds512_k5 0.117 -> 0.110 ms (8: spills and loses)
+#endif
 template <int N, int COB, int RQ, int CQ, int TR, int TC, bool WSM = false>
-__global__ void __launch_bounds__(128, COB == 1 ? 5 : COB == 2 ? 6 : 4)
+__global__ void __launch_bounds__(128, COB == 1 ? SEGB_PAIR_TMA_MINB1 : COB == 2 ? 6 : 4)
     direct_pair_tma_kernel(const __grid_constant__ CUtensorMap tmX, DirectArgs a, const __grid_constant__ PairWeights W) {
     constexpr int NW = N / 2 + 1;
     constexpr int WR = RQ + NW - 1, WC = CQ + NW - 1;
