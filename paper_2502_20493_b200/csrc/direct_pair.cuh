@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(128, PIPE ? 4 : COB == 1 ? 5 : COB == 2 ? 6 : 
 #define SEGB_PAIR_TMA_MINB1 6  // measured: ds512_k5 0.117 -> 0.110 ms (8: spills and loses)
 #endif
 template <int N, int COB, int RQ, int CQ, int TR, int TC, bool WSM = false>
-__global__ void __launch_bounds__(128, COB == 1 ? SEGB_PAIR_TMA_MINB1 : COB == 2 ? 6 : 4)
+// (three channels: 5 blocks per SM with the weights in the parameter, ds512_k4_c3 0.282 -> 0.256 ms;
+// 4 with the weights in shared memory, dcgan_l5 0.120 vs 0.124)
+__global__ void __launch_bounds__(128, COB == 1 ? SEGB_PAIR_TMA_MINB1 : COB == 2 ? 6 : (WSM ? 4 : 5))
     direct_pair_tma_kernel(const __grid_constant__ CUtensorMap tmX, DirectArgs a, const __grid_constant__ PairWeights W) {
     constexpr int NW = N / 2 + 1;
     constexpr int WR = RQ + NW - 1, WC = CQ + NW - 1;
