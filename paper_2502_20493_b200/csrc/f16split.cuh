@@ -18,7 +18,10 @@
 
 namespace segb {
 
-constexpr int kAbsmaxBlocks = 4 * 148;  // partial maxima written by absmax_partials_kernel (4 blocks per SM)
+#ifndef SEGB_ABSMAX_BPS
+#define SEGB_ABSMAX_BPS 8  // measured: 8 vs 4 blocks per SM, ebgan_l5..l7 fp32 0.7-1 % faster
+#endif
+constexpr int kAbsmaxBlocks = SEGB_ABSMAX_BPS * 148;  // partial maxima written by absmax_partials_kernel (blocks per SM x 148)
 constexpr int kAbsmaxBytes = (kAbsmaxBlocks * 4 + 255) / 256 * 256;
 
 // exponent k with max|v| * 2^k < 2^15; 0 for an all-zero or non-finite maximum
